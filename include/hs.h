@@ -1,0 +1,167 @@
+/*
+ * hs.h -- C ABI of libhybridsort.so: the data-parallel hot path of the hybrid
+ * MSD-radix / quicksort / merge sort of Alghamdi & Alaghband, "High
+ * Performance Parallel Sort for Shared and Distributed Memory MIMD"
+ * (arXiv 2003.01216), re-designed for one NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = the paper's text (PAPER.md line n); S:n = SPEC.md line n;
+ * "reading #k" = DESIGN.md §3, the interpretation table for passages the paper
+ * leaves open.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Keys are signed integers, HS_INT32 (4 B) or HS_INT64 (8 B), sorted in
+ *    ascending order.  Key arrays are contiguous, naturally aligned and may
+ *    start at any element offset.
+ *  - Every pointer argument is DEVICE memory owned by the caller.  The
+ *    library never frees, retains or reallocates it.  It may READ (never
+ *    write) up to 15 bytes before the start or past the end of a key array,
+ *    inside the same 16-byte-aligned granule (bulk-copy alignment); such
+ *    bytes never affect a result.
+ *  - Calls are asynchronous: they validate their arguments on the host,
+ *    enqueue kernels on `stream` (NULL = the legacy default stream) of the
+ *    current device, and return.  No call synchronises the host, so a whole
+ *    call can be captured in a CUDA graph.  Scratch (one n-key ping-pong
+ *    buffer, lookback status words, plan and co-rank tables) is taken with
+ *    stream-ordered cudaMallocAsync/cudaFreeAsync from the device's default
+ *    memory pool, whose release threshold the library raises so repeated
+ *    calls do not remap memory.
+ *  - Calls are reentrant and may run concurrently on distinct streams over
+ *    distinct buffers.
+ *  - Validation happens before any launch; on an error nothing is enqueued and
+ *    no output is touched.  Asynchronous device faults surface at the
+ *    caller's next synchronisation, as with any CUDA call.
+ *  - n must satisfy 0 <= n < 2^31 (ABI v1 limit).
+ *
+ * Bucket layout (CSR)
+ * -------------------
+ *  bucket_offsets is a device int64[11]: bucket b (leading decimal digit b)
+ *  occupies [bucket_offsets[b], bucket_offsets[b+1]); [0] = 0, [10] = n.
+ *  The leading digit of a key k with D = num_digits decimal digits is
+ *      d(k) = clamp(floor(k / 10^(D-1)), 0, 9)
+ *  ("divides the data into ten parts based on the most significant
+ *  digit"; keys with fewer than D digits are zero-padded, reading #1; keys
+ *  < 0 or >= 10^D are clamped to bucket 0 / 9, which preserves order, so
+ *  hs_sort sorts ANY int32/int64 input correctly, reading #3).
+ *  num_digits is in [1, 10] for HS_INT32 and [1, 19] for HS_INT64.
+ *
+ * Chunks
+ * ------
+ *  Bucket b of m_b keys is split into c = chunks_per_bucket contiguous chunks
+ *  by partition_even: the first (m_b mod c) chunks hold ceil(m_b/c) keys, the
+ *  rest floor(m_b/c) ("The data is divided among parallel threads";
+ *  rule S:135-143; reading #7).  c must be a power of two in [1, 65536]
+ *  ("the number of threads should be a power of two").
+ */
+#ifndef HS_H_
+#define HS_H_
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+
+typedef enum { HS_INT32 = 0, HS_INT64 = 1 } hs_dtype_t;
+
+typedef enum {
+    HS_OK = 0,
+    HS_ERR_INVALID_VALUE = 1,     /* bad size, NULL pointer, D, c, overlap, misalignment */
+    HS_ERR_UNSUPPORTED_DTYPE = 2, /* dtype outside hs_dtype_t */
+    HS_ERR_OUT_OF_MEMORY = 3,     /* cudaMallocAsync of the scratch failed */
+    HS_ERR_CUDA = 4               /* a CUDA runtime call or launch failed */
+} hs_status_t;
+
+/*
+ * a1-a3: stable one-step MSD radix partition into ten buckets
+ * (§3.4: "implemented one step of MSD-Radix algorithm at the
+ * beginning of the algorithm.  The master node divides the data into ten
+ * parts based on the most significant digit"; stable counting pass S:302,
+ * reading #4; buckets in ascending digit order, reading #5).
+ *
+ *   keys[n]            in : device, not modified.
+ *   out[n]             out: device; keys regrouped by leading digit, keeping
+ *                           input order inside each bucket.  Must not overlap
+ *                           keys (HS_ERR_INVALID_VALUE).
+ *   bucket_offsets[11] out: device int64, CSR offsets (above).  Always
+ *                           required, also for n = 0 (then all zero).
+ *
+ * Result is unique, hence bit-exact against any correct implementation.
+ */
+hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits,
+                             int64_t *bucket_offsets, void *out, cudaStream_t stream);
+
+/*
+ * a4-a5: sort every chunk of every bucket ascending (§3.2 Shared-Parallel
+ * Hybrid Quicksort and Merge Sort, phase 1: "sequential recursive
+ * Quicksort is used to sort the data assigned to each parallel thread").
+ * On the GPU the per-chunk sort is a shared-memory tile sort plus merge-path
+ * merge levels inside the chunk; the result is the same unique array.
+ *
+ *   in[n], out[n]      device; in may equal out (in place); any other overlap
+ *                      is HS_ERR_INVALID_VALUE.  in is read-only unless
+ *                      in == out.
+ *   bucket_offsets[11] in : device int64 CSR offsets (as hs_msd_partition
+ *                      writes them).  Must be non-decreasing with [0] = 0 and
+ *                      [10] = n; this is NOT checked (it lives on the device).
+ *   chunks_per_bucket  c, power of two in [1, 65536].
+ */
+hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtype,
+                           const int64_t *bucket_offsets, int chunks_per_bucket, cudaStream_t stream);
+
+/*
+ * a6: binary-tree merge of each bucket's c sorted chunks (§3.2 phase 2,
+ * "threads sort and merge two children sorted lists (its list and
+ * its neighbor's list) in a binary tree fashion.  This step is repeated using
+ * half of available threads in each round"; schedule S:144-152: round r
+ * merges chunk runs [i, i+2^(r-1)) and [i+2^(r-1), i+2^r) for i mod 2^r = 0).
+ * Buckets are range-disjoint, so no bucket merges with another.
+ * On the GPU every pair of a round is merged at once by merge-path (co-rank)
+ * partitioned CTAs; ties take the left run first (stable-left).
+ *
+ *   in[n], out[n]      device; in may equal out.  Each chunk of in (chunk
+ *                      bounds as above) must be sorted; NOT checked.
+ *   bucket_offsets[11], chunks_per_bucket: as hs_sort_chunks.
+ * With c = 1 there are no rounds: out = in.
+ */
+hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
+                     const int64_t *bucket_offsets, int chunks_per_bucket, cudaStream_t stream);
+
+/*
+ * a1-a7: the whole path, in place (§3.4 Fig 4, P:76-84 with one node,
+ * S:326-334): MSD partition -> sort each chunk -> tree-merge each bucket's
+ * chunks.  Buckets land "to its place in the original array" because
+ * each bucket's last merge level writes straight into keys.
+ *
+ *   keys[n]            in/out: device; ascending on return.
+ *   num_digits, chunks_per_bucket: as above.
+ */
+hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
+                    cudaStream_t stream);
+
+/* Static, human-readable name of a status code. */
+const char *hs_status_string(hs_status_t s);
+
+/* Detail of the last error returned on the calling host thread ("" if none). */
+const char *hs_last_error_message(void);
+
+/* HS_ABI_VERSION of the loaded library. */
+int hs_abi_version(void);
+
+/*
+ * Observability (tests / bench only; not part of the method):
+ * number of kernel launches the most recent successful call on this host
+ * thread enqueued, and the geometry constants compiled into the library:
+ * keys per scatter tile, per tile-sort tile and per merge CTA for dtype.
+ */
+int hs_last_launch_count(void);
+int hs_tile_keys(hs_dtype_t dtype, int which /* 0 scatter, 1 tile sort, 2 merge */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HS_H_ */

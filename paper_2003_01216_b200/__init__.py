@@ -1,0 +1,225 @@
+"""paper_2003_01216_b200 -- B200-native hot path of the hybrid MSD-radix /
+quicksort / merge sort of arXiv 2003.01216 (§3.4).
+
+A thin ctypes binding over libhybridsort.so (C ABI: include/hs.h).  This
+module only marshals arguments: tensors -> device pointers, the current torch
+CUDA stream -> cudaStream_t, status codes -> exceptions.  Every step of the
+method runs in the library's sm_100a kernels.  There is no CPU fallback: if
+the library is missing, or a tensor is not on a CUDA device, calls raise.
+
+Names follow the C ABI (hs_msd_partition, hs_sort_chunks, hs_merge,
+hs_sort); msd_partition / sort_chunks / merge / sort are aliases.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _build
+
+__all__ = [
+    "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_host",
+    "msd_partition", "sort_chunks", "merge", "sort", "sort_host",
+    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS",
+]
+
+HS_INT32, HS_INT64 = 0, 1
+STATUS = {0: "HS_OK", 1: "HS_ERR_INVALID_VALUE", 2: "HS_ERR_UNSUPPORTED_DTYPE", 3: "HS_ERR_OUT_OF_MEMORY", 4: "HS_ERR_CUDA"}
+EXPORTED_SYMBOLS = (
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_status_string",
+    "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
+)
+
+
+class HybridSortError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+def library_path() -> str:
+    return _build.SO
+
+
+_LIB = None
+
+
+def load(path: str | None = None):
+    """Load libhybridsort.so (raises if it has not been built)."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = path or _build.SO
+    if not os.path.exists(p):
+        raise RuntimeError(f"{p} is missing: build it with `python -m paper_2003_01216_b200._build` "
+                           "or __graft_entry__.build(); there is no CPU fallback")
+    lib = ctypes.CDLL(p)
+    vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    lib.hs_msd_partition.argtypes = [vp, i64, ci, ci, vp, vp, vp]
+    lib.hs_sort_chunks.argtypes = [vp, vp, i64, ci, vp, ci, vp]
+    lib.hs_merge.argtypes = [vp, vp, i64, ci, vp, ci, vp]
+    lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
+    for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort"):
+        getattr(lib, f).restype = ci
+    lib.hs_status_string.argtypes = [ci]
+    lib.hs_status_string.restype = ctypes.c_char_p
+    lib.hs_last_error_message.argtypes = []
+    lib.hs_last_error_message.restype = ctypes.c_char_p
+    lib.hs_abi_version.restype = ci
+    lib.hs_last_launch_count.restype = ci
+    lib.hs_tile_keys.argtypes = [ci, ci]
+    lib.hs_tile_keys.restype = ci
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load().hs_last_error_message().decode(errors="replace")
+        raise HybridSortError(rc, msg)
+
+
+def abi_version() -> int:
+    return int(load().hs_abi_version())
+
+
+def last_launch_count() -> int:
+    """Kernel launches enqueued by the last successful call on this thread."""
+    return int(load().hs_last_launch_count())
+
+
+def tile_keys(dtype_code: int, which: int) -> int:
+    return int(load().hs_tile_keys(dtype_code, which))
+
+
+# ------------------------------------------------------------ tensor glue
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.int32:
+        return HS_INT32
+    if t.dtype == torch.int64:
+        return HS_INT64
+    raise TypeError(f"keys must be torch.int32 or torch.int64, got {t.dtype}")
+
+
+def _check_tensor(t, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _stream(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _validate_range(keys, num_digits: int) -> None:
+    """SPEC S:294 KeyOutOfRange: optional check that 0 <= k < 10^D (reading #3)."""
+    torch = _torch()
+    hi = 10 ** num_digits
+    bad = (keys < 0) | (keys >= hi) if hi <= torch.iinfo(keys.dtype).max else (keys < 0)
+    if bool(bad.any()):
+        idx = int(torch.nonzero(bad)[0, 0])
+        raise ValueError(f"key at index {idx} ({int(keys[idx])}) is outside [0, 10^{num_digits})")
+
+
+def hs_msd_partition(keys, num_digits: int, out=None, bucket_offsets=None, stream=None, validate: bool = False):
+    """Stable one-step MSD partition.  Returns (out, bucket_offsets[11])."""
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    dt = _dtype_code(keys)
+    if validate:
+        _validate_range(keys, num_digits)
+    if out is None:
+        out = torch.empty_like(keys)
+    if bucket_offsets is None:
+        bucket_offsets = torch.empty(11, dtype=torch.int64, device=keys.device)
+    _check_tensor(out, "out")
+    _check_tensor(bucket_offsets, "bucket_offsets")
+    if out.dtype != keys.dtype or out.numel() != keys.numel():
+        raise ValueError("out must match keys in dtype and size")
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    with torch.cuda.device(keys.device):
+        _check(load().hs_msd_partition(keys.data_ptr(), keys.numel(), dt, num_digits, bucket_offsets.data_ptr(),
+                                       out.data_ptr(), _stream(stream)))
+    return out, bucket_offsets
+
+
+def hs_sort_chunks(x, bucket_offsets, chunks_per_bucket: int = 8, out=None, stream=None):
+    """Sort every chunk of every bucket.  out=x sorts in place."""
+    torch = _torch()
+    _check_tensor(x, "x")
+    _check_tensor(bucket_offsets, "bucket_offsets")
+    dt = _dtype_code(x)
+    if out is None:
+        out = torch.empty_like(x)
+    _check_tensor(out, "out")
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    with torch.cuda.device(x.device):
+        _check(load().hs_sort_chunks(x.data_ptr(), out.data_ptr(), x.numel(), dt, bucket_offsets.data_ptr(),
+                                     chunks_per_bucket, _stream(stream)))
+    return out
+
+
+def hs_merge(x, bucket_offsets, chunks_per_bucket: int = 8, out=None, stream=None):
+    """Binary-tree merge of each bucket's sorted chunks.  out=x merges in place."""
+    torch = _torch()
+    _check_tensor(x, "x")
+    _check_tensor(bucket_offsets, "bucket_offsets")
+    dt = _dtype_code(x)
+    if out is None:
+        out = torch.empty_like(x)
+    _check_tensor(out, "out")
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    with torch.cuda.device(x.device):
+        _check(load().hs_merge(x.data_ptr(), out.data_ptr(), x.numel(), dt, bucket_offsets.data_ptr(),
+                               chunks_per_bucket, _stream(stream)))
+    return out
+
+
+def hs_sort(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None, validate: bool = False):
+    """Whole path in place: partition -> chunk sort -> tree merge.  Returns keys."""
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    dt = _dtype_code(keys)
+    if validate:
+        _validate_range(keys, num_digits)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket, _stream(stream)))
+    return keys
+
+
+def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=None, out=None):
+    """End-to-end convenience: pinned host keys -> H2D -> hs_sort -> D2H.
+
+    host_keys is a (preferably pinned) CPU torch tensor; the sorted keys are
+    copied into ``out`` (a CPU tensor, default: a new pinned one)."""
+    torch = _torch()
+    dev = torch.device(device or "cuda")
+    d = host_keys.to(dev, non_blocking=True)
+    hs_sort(d, num_digits, chunks_per_bucket)
+    if out is None:
+        out = torch.empty_like(host_keys, pin_memory=True)
+    out.copy_(d, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return out
+
+
+msd_partition = hs_msd_partition
+sort_chunks = hs_sort_chunks
+merge = hs_merge
+sort = hs_sort
+sort_host = hs_sort_host

@@ -1,0 +1,367 @@
+// hs_api.cu -- the C ABI of libhybridsort.so (declared and documented in
+// include/hs.h): argument validation, stream-ordered scratch, and the launch
+// sequence of each entry point.  Every step of the method runs in the
+// kernels of hs_kernels.cu; this file only sequences them.
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "hs.h"
+#include "hs_device.cuh"
+#include "hs_launch.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+hs_status_t fail(hs_status_t s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+hs_status_t fail(hs_status_t s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+hs_status_t cuda_fail(cudaError_t e, const char *what) {
+    return fail(HS_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+constexpr int kMaxDevices = 64;
+std::once_flag g_dev_once[kMaxDevices];
+int g_num_sms[kMaxDevices];
+
+cudaError_t device_setup(int *num_sms) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    cudaError_t err = cudaSuccess;
+    std::call_once(g_dev_once[dev], [&]() {
+        int sms = 0;
+        err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = sms > 0 ? sms : 148;
+        // keep freed scratch in the pool so repeated calls do not remap memory
+        cudaMemPool_t pool;
+        if (err == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    if (err != cudaSuccess) return err;
+    *num_sms = g_num_sms[dev];
+    return cudaSuccess;
+}
+
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int ksize(hs_dtype_t dt) { return dt == HS_INT32 ? 4 : 8; }
+
+bool overlap(const void *a, const void *b, size_t bytes) {
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + bytes && y < x + bytes;
+}
+
+int ceil_log2(long long x) {
+    int r = 0;
+    while ((1LL << r) < x) ++r;
+    return r;
+}
+
+hs_status_t check_common(int64_t n, hs_dtype_t dt) {
+    if (dt != HS_INT32 && dt != HS_INT64) return fail(HS_ERR_UNSUPPORTED_DTYPE, "dtype %d is not HS_INT32/HS_INT64", (int)dt);
+    if (n < 0 || n >= (1LL << 31)) return fail(HS_ERR_INVALID_VALUE, "n = %lld outside [0, 2^31)", (long long)n);
+    return HS_OK;
+}
+
+hs_status_t check_ptr(const void *p, int64_t n, hs_dtype_t dt, const char *name) {
+    if (n > 0 && p == nullptr) return fail(HS_ERR_INVALID_VALUE, "%s is NULL with n > 0", name);
+    if (p && ((uintptr_t)p % ksize(dt)) != 0) return fail(HS_ERR_INVALID_VALUE, "%s is not %d-byte aligned", name, ksize(dt));
+    return HS_OK;
+}
+
+hs_status_t check_digits(int D, hs_dtype_t dt) {
+    int hi = dt == HS_INT32 ? 10 : 19;
+    if (D < 1 || D > hi) return fail(HS_ERR_INVALID_VALUE, "num_digits = %d outside [1, %d]", D, hi);
+    return HS_OK;
+}
+
+hs_status_t check_chunks(int c, int *log2c) {
+    if (c < 1 || c > 65536 || (c & (c - 1)) != 0)
+        return fail(HS_ERR_INVALID_VALUE, "chunks_per_bucket = %d is not a power of two in [1, 65536] (P:80)", c);
+    *log2c = ceil_log2(c);
+    return HS_OK;
+}
+
+hs_status_t check_inout(const void *in, const void *out, int64_t n, hs_dtype_t dt) {
+    if (in != out && n > 0 && overlap(in, out, (size_t)n * ksize(dt)))
+        return fail(HS_ERR_INVALID_VALUE, "in and out overlap without being equal");
+    return HS_OK;
+}
+
+// 10^(D-1) and the multiply-high magic floor((2^w - 1) / div) (K1).
+void digit_params(int D, hs_dtype_t dt, unsigned long long *div, unsigned long long *magic) {
+    unsigned long long d = 1;
+    for (int i = 1; i < D; ++i) d *= 10ull;
+    *div = d;
+    *magic = dt == HS_INT32 ? (0xFFFFFFFFull / d) : (~0ull / d);
+}
+
+// Scratch for one call: [S keys][Ctl][lookback status][co-ranks], one
+// stream-ordered allocation.  Ctl + status are zeroed by one memset.
+struct Workspace {
+    char *base = nullptr;
+    void *S = nullptr;
+    hs::Ctl *ctl = nullptr;
+    unsigned long long *status = nullptr;
+    int *corank = nullptr;
+    size_t zero_bytes = 0;
+};
+
+hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t corank_words, cudaStream_t st) {
+    size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
+    size_t c = round_up(sizeof(hs::Ctl), 256);
+    size_t z = round_up(status_words * 8, 256);
+    size_t k = round_up(corank_words * 4, 256);
+    size_t total = a + c + z + k;
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, total, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed: %s", total, cudaGetErrorString(e));
+    }
+    w->base = (char *)p;
+    w->S = s_bytes ? w->base : nullptr;
+    w->ctl = (hs::Ctl *)(w->base + a);
+    w->status = (unsigned long long *)(w->base + a + c);
+    w->corank = (int *)(w->base + a + c + z);
+    w->zero_bytes = c + z;
+    return HS_OK;
+}
+
+#define HS_TRY_CUDA(expr, what)                                   \
+    do {                                                          \
+        cudaError_t _e = (expr);                                  \
+        ++launches;                                               \
+        if (_e != cudaSuccess) {                                  \
+            if (ws.base) cudaFreeAsync(ws.base, stream);          \
+            return cuda_fail(_e, what);                           \
+        }                                                         \
+    } while (0)
+
+hs_status_t finish(Workspace &ws, cudaStream_t stream, int launches) {
+    cudaError_t e = cudaFreeAsync(ws.base, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    g_launches = launches;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+// Merge levels the host must launch: each bucket runs L[b] <= this many
+// (k[b] <= ceil(log2(ceil(ceil(n/c)/T)))); levels with no active bucket
+// cost one near-empty launch pair.
+int level_bound(long long n, int log2c, int T, int with_tiles, int with_tree) {
+    int k = 0;
+    if (with_tiles) {
+        long long c = 1LL << log2c;
+        long long cm = (n + c - 1) / c;
+        long long t = (cm + T - 1) / T;
+        k = t > 1 ? ceil_log2(t) : 0;
+    }
+    return k + (with_tree ? log2c : 0);
+}
+
+long long tile_bound(long long n, long long c, int T) { return 2 * ((n + T - 1) / T) + 50 * c; }
+
+}  // namespace
+
+extern "C" {
+
+const char *hs_status_string(hs_status_t s) {
+    switch (s) {
+        case HS_OK: return "HS_OK";
+        case HS_ERR_INVALID_VALUE: return "HS_ERR_INVALID_VALUE";
+        case HS_ERR_UNSUPPORTED_DTYPE: return "HS_ERR_UNSUPPORTED_DTYPE";
+        case HS_ERR_OUT_OF_MEMORY: return "HS_ERR_OUT_OF_MEMORY";
+        case HS_ERR_CUDA: return "HS_ERR_CUDA";
+    }
+    return "HS_ERR_UNKNOWN";
+}
+
+const char *hs_last_error_message(void) { return g_err; }
+int hs_abi_version(void) { return HS_ABI_VERSION; }
+int hs_last_launch_count(void) { return g_launches; }
+
+int hs_tile_keys(hs_dtype_t dtype, int which) {
+    if (dtype != HS_INT32 && dtype != HS_INT64) return 0;
+    return hs::tile_keys((int)dtype, which);
+}
+
+hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int64_t *bucket_offsets,
+                             void *out, cudaStream_t stream) {
+    hs_status_t s;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if ((s = check_ptr(out, n, dtype, "out")) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if (((uintptr_t)bucket_offsets & 7) != 0) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is not 8-byte aligned");
+    if (n > 0 && overlap(keys, out, (size_t)n * ksize(dtype)))
+        return fail(HS_ERR_INVALID_VALUE, "keys and out overlap (the partition is out of place)");
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+
+    const int dt = (int)dtype;
+    const int Tp = hs::tile_keys(dt, 0);
+    const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
+    const long long tiles = (n + h + Tp - 1) / Tp;
+    unsigned long long div, magic;
+    digit_params(num_digits, dtype, &div, &magic);
+
+    Workspace ws;
+    if ((s = ws_alloc(&ws, 0, (size_t)tiles * 10, 0, stream)) != HS_OK) return s;
+    int launches = 0;
+    HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
+    HS_TRY_CUDA(hs::launch_histogram(dt, keys, (int)n, h, div, magic, ws.ctl, (long long *)bucket_offsets, -1, 0, sms,
+                                     stream),
+                "K1 histogram");
+    if (n > 0)
+        HS_TRY_CUDA(hs::launch_scatter(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.status, stream), "K3 scatter");
+    return finish(ws, stream, launches - 1);  // the memset is not one of our kernels
+}
+
+hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
+                    cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+
+    const int dt = (int)dtype;
+    const int Tp = hs::tile_keys(dt, 0), T = hs::tile_keys(dt, 1), TM = hs::tile_keys(dt, 2);
+    const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
+    const long long ptiles = (n + h + Tp - 1) / Tp;
+    const long long nblocks = (n + TM - 1) / TM;
+    unsigned long long div, magic;
+    digit_params(num_digits, dtype, &div, &magic);
+
+    Workspace ws;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)ptiles * 10, (size_t)nblocks + 2, stream)) != HS_OK)
+        return s;
+    int launches = 0;
+    const hs::Plan *plan = &ws.ctl->plan;
+    HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
+    // a1: histogram + bucket offsets + plan (last CTA)
+    HS_TRY_CUDA(hs::launch_histogram(dt, keys, (int)n, h, div, magic, ws.ctl, nullptr, hs::kPlanSort, log2c, sms, stream),
+                "K1 histogram");
+    // a2+a3: stable scatter keys -> S
+    HS_TRY_CUDA(hs::launch_scatter(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.status, stream), "K3 scatter");
+    // a5: leaf-tile sort S -> (keys | S) per bucket parity
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, tile_bound(n, chunks_per_bucket, T), stream),
+                "K5 tile sort");
+    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
+    const int L = level_bound(n, log2c, T, 1, 1);
+    for (int lv = 0; lv < L; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, lv, (int)n, stream), "K6 merge level");
+        ++launches;  // partition + merge
+    }
+    return finish(ws, stream, launches - 1);
+}
+
+hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
+                           int chunks_per_bucket, cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(in, n, dtype, "in")) != HS_OK) return s;
+    if ((s = check_ptr(out, n, dtype, "out")) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if ((s = check_inout(in, out, n, dtype)) != HS_OK) return s;
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    const int dt = (int)dtype;
+    const int T = hs::tile_keys(dt, 1), TM = hs::tile_keys(dt, 2);
+    const long long nblocks = (n + TM - 1) / TM;
+
+    Workspace ws;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    int launches = 0;
+    const hs::Plan *plan = &ws.ctl->plan;
+    HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanChunks, T, stream), "K4 plan");
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, in, out, ws.S, tile_bound(n, chunks_per_bucket, T), stream), "K5 tile sort");
+    const int L = level_bound(n, log2c, T, 1, 0);
+    for (int lv = 0; lv < L; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, lv, (int)n, stream), "K6 merge level");
+        ++launches;
+    }
+    return finish(ws, stream, launches);
+}
+
+hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
+                     int chunks_per_bucket, cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(in, n, dtype, "in")) != HS_OK) return s;
+    if ((s = check_ptr(out, n, dtype, "out")) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if ((s = check_inout(in, out, n, dtype)) != HS_OK) return s;
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    const int dt = (int)dtype;
+    const int TM = hs::tile_keys(dt, 2);
+    const long long nblocks = (n + TM - 1) / TM;
+    int launches = 0;
+    Workspace ws;
+    if (log2c == 0) {  // c = 1: zero rounds, out = in
+        if (in != out) HS_TRY_CUDA(hs::launch_copy(dt, in, out, n, sms, stream), "K7 copy");
+        g_launches = launches;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    const hs::Plan *plan = &ws.ctl->plan;
+    HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanMerge, 1, stream), "K4 plan");
+    const void *src0 = in;
+    if (in == out) {
+        src0 = nullptr;
+        // level 0 must read the buffer its parity names: S when the round
+        // count is odd, so the in-place case starts with one copy (K7).
+        if (log2c & 1) HS_TRY_CUDA(hs::launch_copy(dt, in, ws.S, n, sms, stream), "K7 copy");
+    }
+    for (int lv = 0; lv < log2c; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, lv, (int)n, stream), "K6 merge level");
+        ++launches;
+    }
+    return finish(ws, stream, launches);
+}
+
+}  // extern "C"

@@ -1,0 +1,287 @@
+// hs_device.cuh -- device-side building blocks shared by the sm_100a kernels
+// of libhybridsort.so: key traits, the leading-decimal-digit function, the
+// per-call plan (bucket / chunk / leaf-tile geometry) and thin PTX wrappers
+// (bulk async copy, mbarrier, relaxed gpu-scope loads/stores).
+//
+// Nothing here is shared with oracle/ (the CPU checker).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hs {
+
+// --------------------------------------------------------------- key traits
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<int32_t> {
+    using U = uint32_t;
+    static constexpr int32_t kMax = 0x7fffffff;
+};
+template <>
+struct KeyTraits<int64_t> {
+    using U = unsigned long long;
+    static constexpr int64_t kMax = 0x7fffffffffffffffLL;
+};
+
+// Leading decimal digit of a D-digit key, d(k) = clamp(floor(k / 10^(D-1)), 0, 9)
+// (reading #1 zero-padding, #3 clamping).  Division by the runtime
+// constant div = 10^(D-1) is a multiply-high by magic = floor((2^w - 1) / div)
+// plus one correction step: for 0 <= k < 2^(w-1) the estimate is q or q-1
+// (K1), so r = k - est*div lies in [0, 2 div).
+template <typename K>
+struct DigitParams {
+    typename KeyTraits<K>::U div;
+    typename KeyTraits<K>::U magic;
+};
+
+__device__ __forceinline__ int msd_digit(int32_t k, const DigitParams<int32_t> &p) {
+    if (k < 0) return 0;
+    uint32_t u = (uint32_t)k;
+    uint32_t q = __umulhi(u, p.magic);
+    uint32_t r = u - q * p.div;
+    q += (r >= p.div) ? 1u : 0u;
+    return (int)(q < 9u ? q : 9u);
+}
+
+__device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &p) {
+    if (k < 0) return 0;
+    unsigned long long u = (unsigned long long)k;
+    unsigned long long q = __umul64hi(u, p.magic);
+    unsigned long long r = u - q * p.div;
+    q += (r >= p.div) ? 1ull : 0ull;
+    return (int)(q < 9ull ? q : 9ull);
+}
+
+// ------------------------------------------------------------------- plan
+// Geometry of one call, computed on the device (no host sync).
+//  * bucket b = [off[b], off[b+1]).
+//  * chunks: partition_even(m_b, c).
+//  * leaf tiles: each chunk is split by partition_even into 2^k[b] leaves of
+//    at most T keys (T = tile-sort capacity); k[b] is chosen from the largest
+//    chunk, so every chunk of a bucket has the same power-of-two leaf count
+//    and the bucket's merge tree over its c * 2^k[b] leaves is perfect (no
+//    pass-through runs, hence no copies).
+//  * merge level lam of bucket b merges leaf runs [2p 2^lam, (2p+1) 2^lam) and
+//    [(2p+1) 2^lam, (2p+2) 2^lam).  Levels lam < k[b] are the in-chunk
+//    merges of a5; levels k[b] .. k[b]+log2 c - 1 are the paper's tree merge
+//    of the chunks (a6).
+//  * L[b] = number of merge levels this call runs for bucket b.
+struct Plan {
+    long long off[11];
+    long long tile_prefix[11];  // exclusive prefix of leaf counts (c << k[b])
+    int k[10];
+    int L[10];
+    int log2c;
+    int Lmax;
+};
+
+enum PlanMode { kPlanSort = 0, kPlanChunks = 1, kPlanMerge = 2 };
+
+__device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
+    int r = 0;
+    while ((1LL << r) < x) ++r;
+    return r;
+}
+
+// One thread fills *P from off[11].
+__device__ inline void compute_plan(Plan *P, const long long *off, int log2c, int mode, int tile_keys) {
+    long long c = 1LL << log2c;
+    long long acc = 0;
+    int lmax = 0;
+    for (int b = 0; b < 10; ++b) {
+        long long m = off[b + 1] - off[b];
+        int k = 0;
+        if (mode != kPlanMerge) {
+            long long cm = (m + c - 1) / c;                        // largest chunk
+            long long tiles = (cm + tile_keys - 1) / tile_keys;    // leaves it needs
+            k = tiles > 1 ? ceil_log2_ll(tiles) : 0;
+        }
+        int L = (mode == kPlanSort) ? k + log2c : (mode == kPlanChunks ? k : log2c);
+        P->off[b] = off[b];
+        P->k[b] = k;
+        P->L[b] = L;
+        P->tile_prefix[b] = acc;
+        acc += (c << k);
+        lmax = L > lmax ? L : lmax;
+    }
+    P->off[10] = off[10];
+    P->tile_prefix[10] = acc;
+    P->log2c = log2c;
+    P->Lmax = lmax;
+}
+
+// Start of part i of partition_even(m, p = 2^lg): i*floor(m/p) + min(i, m mod p).
+__device__ __forceinline__ long long part_start(long long m, int lg, long long i) {
+    long long q = m >> lg, r = m & ((1LL << lg) - 1);
+    return i * q + (i < r ? i : r);
+}
+
+// Index of the part of partition_even(m, 2^lg) containing y (0 <= y < m).
+__device__ __forceinline__ long long part_index(long long m, int lg, long long y) {
+    long long q = m >> lg, r = m & ((1LL << lg) - 1);
+    long long B = r * (q + 1);
+    // positions < 2^31 (ABI limit): 32-bit unsigned division is exact here
+    if (y < B) return (long long)((unsigned)y / (unsigned)(q + 1));
+    return r + (long long)((unsigned)(y - B) / (unsigned)q);
+}
+
+// Absolute start of leaf i of bucket b (0 <= i <= c << k[b]).
+__device__ __forceinline__ long long leaf_start(const Plan &P, int b, long long i) {
+    long long m = P.off[b + 1] - P.off[b];
+    int k = P.k[b];
+    long long j = i >> k, t = i & ((1LL << k) - 1);
+    long long cs = part_start(m, P.log2c, j);
+    if (t == 0) return P.off[b] + cs;
+    long long q = m >> P.log2c, r = m & ((1LL << P.log2c) - 1);
+    long long len = q + (j < r ? 1 : 0);
+    return P.off[b] + cs + part_start(len, k, t);
+}
+
+// Leaf of bucket b containing absolute position x (off[b] <= x < off[b+1]).
+__device__ __forceinline__ long long leaf_of(const Plan &P, int b, long long x) {
+    long long m = P.off[b + 1] - P.off[b];
+    int k = P.k[b];
+    long long y = x - P.off[b];
+    long long j = part_index(m, P.log2c, y);
+    if (k == 0) return j;
+    long long q = m >> P.log2c, r = m & ((1LL << P.log2c) - 1);
+    long long len = q + (j < r ? 1 : 0);
+    long long z = y - part_start(m, P.log2c, j);
+    return (j << k) + part_index(len, k, z);
+}
+
+__device__ __forceinline__ int bucket_of(const Plan &P, long long x) {
+    int b = 0;
+    while (b < 9 && x >= P.off[b + 1]) ++b;
+    return b;
+}
+
+// Pair geometry at merge level lam for the pair containing leaf lf.
+struct PairGeom {
+    long long a_lo, b_lo, b_hi;
+};
+__device__ __forceinline__ PairGeom pair_of(const Plan &P, int b, long long lf, int lam) {
+    long long p = lf >> (lam + 1);
+    PairGeom g;
+    g.a_lo = leaf_start(P, b, p << (lam + 1));
+    g.b_lo = leaf_start(P, b, ((2 * p + 1) << lam));
+    g.b_hi = leaf_start(P, b, (p + 1) << (lam + 1));
+    return g;
+}
+
+// Which buffer holds bucket b's runs before level lam: the last level
+// (L-1) must write the final buffer F, so the data before level lam sits in
+// F iff (L - lam) is even.
+template <typename K>
+__device__ __forceinline__ K *level_src(const Plan &P, int b, int lam, K *F, K *S) {
+    return ((P.L[b] - lam) & 1) == 0 ? F : S;
+}
+template <typename K>
+__device__ __forceinline__ K *level_dst(const Plan &P, int b, int lam, K *F, K *S) {
+    return ((P.L[b] - 1 - lam) & 1) == 0 ? F : S;
+}
+
+// Per-call control block (zeroed by one memset before the first kernel).
+struct Ctl {
+    unsigned long long hist[10];
+    unsigned int done;
+    unsigned int ticket;
+    long long off[11];
+    Plan plan;
+};
+
+// --------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk async copy (TMA engine) global -> shared, completion counted in
+// bytes on the mbarrier.  dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int4 ld_stream_v4(const void *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Padded shared-memory index: one spare word per 32 keys so that a thread
+// reading VT consecutive keys (blocked layout) and a warp reading 32
+// consecutive keys (striped layout) are both bank-conflict free.
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 5); }
+
+template <typename K>
+__device__ __forceinline__ void cas(K &a, K &b) {
+    K lo = a < b ? a : b;
+    K hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+
+// Batcher odd-even merge sort network on N registers (all indices are
+// compile-time after unrolling, so v stays in registers).
+template <int N, typename K>
+__device__ __forceinline__ void oddeven_sort(K (&v)[N]) {
+#pragma unroll
+    for (int p = 1; p < N; p <<= 1) {
+#pragma unroll
+        for (int k = p; k >= 1; k >>= 1) {
+#pragma unroll
+            for (int j = k % p; j + k < N; j += 2 * k) {
+#pragma unroll
+                for (int i = 0; i < k; ++i) {
+                    if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p)) cas(v[i + j], v[i + j + k]);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace hs

@@ -1,0 +1,343 @@
+"""GPU parity: the CUDA path (through the C ABI via the ctypes binding) is
+bit-exact against the CPU oracle on the same seeded inputs.
+
+Every API's result is unique for keys-only data, so the bar
+is exact equality of every element (integer work).  Sizes span several
+tiles of every kernel plus ragged tails; edge cases cover empty / tiny
+inputs, misaligned sub-tensor pointers, every digit boundary, clamped
+out-of-range keys, skewed buckets, all-equal keys, and c in {1..64}.
+Full-size configs compare against the oracle element-by-element where the
+oracle finishes in seconds (C1, C2, C4) and on oracle-computed samples plus
+size-independent invariants otherwise (C3, C5).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workload as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2003_01216_b200 as hs  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def _tiles(code):
+    try:
+        return tuple(hs.tile_keys(code, i) for i in range(3))
+    except RuntimeError:  # library not built: collection must still work on CPU
+        return (8192, 8192, 4096) if code == 0 else (4096, 4096, 2048)
+
+
+Tp32, T32, TM32 = _tiles(0)
+Tp64, T64, TM64 = _tiles(1)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    hs.load()
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t) -> np.ndarray:
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def assert_same(got: np.ndarray, ref: np.ndarray, what: str = ""):
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    if not np.array_equal(got, ref):
+        bad = np.nonzero(got != ref)[0]
+        raise AssertionError(f"{what}: {bad.size} mismatches, first at {bad[0]}: got {got[bad[0]]} want {ref[bad[0]]}")
+
+
+def rand_keys(n, hi, seed, dtype):
+    return W.uniform(n, seed, hi, dtype=dtype)
+
+
+SIZES32 = [0, 1, 2, 31, 1000, Tp32 - 1, Tp32, Tp32 + 1, 3 * Tp32 + 17, 100_003, 1 << 20]
+SIZES64 = [0, 1, 5, Tp64 - 1, Tp64 + 1, 5 * Tp64 + 3, 70_001]
+
+
+# ------------------------------------------------------------ msd_partition
+@pytest.mark.parametrize("n", SIZES32)
+def test_partition_int32_sizes(n):
+    keys = rand_keys(n, 10**6, 100 + n, np.int32)
+    out, off = hs.hs_msd_partition(dev(keys), 6)
+    ref, ref_off = O.msd_partition(keys, 6)
+    assert_same(host(off), ref_off, "offsets")
+    assert_same(host(out), ref.astype(np.int32), "partition")
+
+
+@pytest.mark.parametrize("n", SIZES64)
+def test_partition_int64_sizes(n):
+    keys = rand_keys(n, 10**18, 200 + n, np.int64)
+    out, off = hs.hs_msd_partition(dev(keys), 18)
+    ref, ref_off = O.msd_partition(keys, 18)
+    assert_same(host(off), ref_off, "offsets")
+    assert_same(host(out), ref.astype(np.int64), "partition")
+
+
+@pytest.mark.parametrize("dtype,D", [(np.int32, d) for d in range(1, 11)] + [(np.int64, d) for d in range(1, 20)])
+def test_partition_digit_boundaries(dtype, D):
+    """Every d*10^(D-1) - 1 / d*10^(D-1) boundary, 0, 10^D - 1, plus clamped keys."""
+    info = np.iinfo(dtype)
+    base = 10 ** (D - 1)
+    ks = [0, 1, info.max, info.min, -1]
+    for d in range(0, 11):
+        for e in (-2, -1, 0, 1):
+            v = d * base + e
+            if info.min <= v <= info.max:
+                ks.append(v)
+    keys = np.array(ks * 97, dtype=dtype)
+    np.random.default_rng(D).shuffle(keys)
+    out, off = hs.hs_msd_partition(dev(keys), D)
+    ref, ref_off = O.msd_partition(keys, D)
+    assert_same(host(off), ref_off, "offsets")
+    assert_same(host(out), ref.astype(dtype), "partition")
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3, 5])
+def test_partition_misaligned_views(shift):
+    n = 3 * Tp32 + 11
+    base = rand_keys(n + 8, 10**9, 7, np.int32)
+    full = dev(base)
+    view = full[shift:shift + n]
+    out_full = torch.empty(n + 8, dtype=torch.int32, device=DEV)
+    out = out_full[3:3 + n]
+    hs.hs_msd_partition(view, 9, out=out)
+    ref, _ = O.msd_partition(base[shift:shift + n], 9)
+    assert_same(host(out), ref.astype(np.int32), "misaligned partition")
+
+
+def test_partition_c1_full():
+    keys = W.generate("C1")
+    out, off = hs.hs_msd_partition(dev(keys), 6)
+    ref, ref_off = O.msd_partition(keys, 6)
+    assert_same(host(off), ref_off)
+    assert_same(host(out), ref.astype(np.int32))
+
+
+def test_partition_worked_examples(golden):
+    for ex in golden["msd_partition"]:
+        keys = np.array(ex["keys"], dtype=np.int32)
+        out, off = hs.hs_msd_partition(dev(keys), ex["D"])
+        assert host(off).tolist() == ex["offsets"]
+        assert host(out).tolist() == ex["partitioned"]
+
+
+# -------------------------------------------------------------- sort_chunks
+def skewed_keys(n, seed):
+    """Unbalanced buckets: most keys in digits 2-3, a few in the others (C4 shape)."""
+    rng = np.random.default_rng(seed)
+    k = rng.integers(2 * 10**8, 4 * 10**8, size=n)
+    few = rng.random(n) < 0.08
+    k[few] = rng.integers(0, 10**9, size=int(few.sum()))
+    dup = rng.random(n) < 0.2
+    k[dup] = rng.integers(0, 1024, size=int(dup.sum())) * 976_561
+    return k.astype(np.int32)
+
+
+@pytest.mark.parametrize("c", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_sort_chunks(c, inplace):
+    keys = skewed_keys(300_007, c)
+    part, off = O.msd_partition(keys, 9)
+    part = part.astype(np.int32)
+    x = dev(part)
+    d_off = dev(off)
+    out = hs.hs_sort_chunks(x, d_off, c, out=x if inplace else None)
+    ref = O.sort_chunks(part, off, c)
+    assert_same(host(out), ref, f"sort_chunks c={c}")
+    if not inplace:
+        assert_same(host(x), part, "input untouched")
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, T32 - 1, T32 + 1, 8 * T32 + 5])
+def test_sort_chunks_sizes(n):
+    keys = rand_keys(n, 10**9, 300 + n, np.int32)
+    part, off = O.msd_partition(keys, 9)
+    out = hs.hs_sort_chunks(dev(part.astype(np.int32)), dev(off), 8)
+    assert_same(host(out), O.sort_chunks(part, off, 8).astype(np.int32))
+
+
+def test_sort_chunks_int64():
+    keys = rand_keys(123_457, 10**18, 5, np.int64)
+    part, off = O.msd_partition(keys, 18)
+    out = hs.hs_sort_chunks(dev(part), dev(off), 4)
+    assert_same(host(out), O.sort_chunks(part, off, 4))
+
+
+def test_sort_chunks_golden(golden):
+    for ex in golden["sort_chunks"]:
+        x = dev(np.array(ex["partitioned"], dtype=np.int32))
+        off = dev(np.array(ex["offsets"], dtype=np.int64))
+        out = hs.hs_sort_chunks(x, off, ex["c"])
+        assert host(out).tolist() == ex["chunk_sorted"]
+        assert host(hs.hs_merge(out, off, ex["c"])).tolist() == ex["merged"]
+
+
+# -------------------------------------------------------------------- merge
+@pytest.mark.parametrize("c", [1, 2, 4, 8, 16, 64])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_merge(c, inplace):
+    keys = skewed_keys(200_003, 10 + c)
+    part, off = O.msd_partition(keys, 9)
+    cs = O.sort_chunks(part, off, c).astype(np.int32)
+    x = dev(cs)
+    out = hs.hs_merge(x, dev(off), c, out=x if inplace else None)
+    assert_same(host(out), O.merge(cs, off, c), f"merge c={c}")
+    if not inplace:
+        assert_same(host(x), cs, "input untouched")
+
+
+def test_merge_int64_odd_rounds_inplace():
+    keys = rand_keys(99_999, 10**18, 9, np.int64)
+    part, off = O.msd_partition(keys, 18)
+    cs = O.sort_chunks(part, off, 8)
+    x = dev(cs)
+    hs.hs_merge(x, dev(off), 8, out=x)
+    assert_same(host(x), O.merge(cs, off, 8))
+
+
+# --------------------------------------------------------------------- sort
+@pytest.mark.parametrize("n", SIZES32 + [2 * 8 * T32 + 1])
+def test_sort_int32_sizes(n):
+    keys = rand_keys(n, 10**6, 400 + n, np.int32)
+    d = dev(keys)
+    hs.hs_sort(d, 6, 8)
+    assert_same(host(d), O.sort(keys, 6, 8), f"sort n={n}")
+
+
+@pytest.mark.parametrize("n", SIZES64)
+def test_sort_int64_sizes(n):
+    keys = rand_keys(n, 10**18, 500 + n, np.int64)
+    d = dev(keys)
+    hs.hs_sort(d, 18, 8)
+    assert_same(host(d), O.sort(keys, 18, 8), f"sort64 n={n}")
+
+
+@pytest.mark.parametrize("c", [1, 2, 4, 16, 64])
+def test_sort_chunk_counts(c):
+    keys = skewed_keys(250_001, 20 + c)
+    d = dev(keys)
+    hs.hs_sort(d, 9, c)
+    assert_same(host(d), O.sort(keys, 9, c), f"sort c={c}")
+
+
+@pytest.mark.parametrize("kind", ["equal", "sorted", "reversed", "two_values", "clamped", "negative"])
+def test_sort_degenerate(kind):
+    n = 3 * T32 * 8 + 123
+    if kind == "equal":
+        keys = np.full(n, 555_555, dtype=np.int32)
+    elif kind == "sorted":
+        keys = np.arange(n, dtype=np.int32) * 7
+    elif kind == "reversed":
+        keys = (np.arange(n, dtype=np.int32) * 7)[::-1].copy()
+    elif kind == "two_values":
+        keys = np.where(np.arange(n) % 3 == 0, 10, 999_999).astype(np.int32)
+    elif kind == "clamped":   # keys >= 10^D and < 0 are clamped (reading #3); still a full sort
+        keys = W.uniform(n, 3, 2**31 - 1, dtype=np.int32)
+    else:
+        keys = (W.uniform(n, 4, 2**31 - 1, dtype=np.int32).astype(np.int64) - 2**30).astype(np.int32)
+    d = dev(keys)
+    hs.hs_sort(d, 6, 8)
+    got = host(d)
+    assert_same(got, O.sort(keys, 6, 8), kind)
+    assert_same(got, np.sort(keys), kind + " (library special case)")
+
+
+def test_sort_worked_examples():
+    for keys, D, c, expect in [([345, 7, 999, 100], 3, 2, [7, 100, 345, 999]),
+                               ([512, 37, 508, 999, 500, 41, 512, 0, 730, 105], 3, 2,
+                                [0, 37, 41, 105, 500, 508, 512, 512, 730, 999])]:
+        d = dev(np.array(keys, dtype=np.int32))
+        hs.hs_sort(d, D, c)
+        assert host(d).tolist() == expect
+
+
+def test_sort_misaligned_view():
+    n = 5 * T32 + 3
+    base = rand_keys(n + 4, 10**9, 77, np.int32)
+    full = dev(base)
+    view = full[1:1 + n]
+    hs.hs_sort(view, 9, 8)
+    got = host(full)
+    assert got[0] == base[0] and np.array_equal(got[1 + n:], base[1 + n:])
+    assert_same(got[1:1 + n], O.sort(base[1:1 + n], 9, 8))
+
+
+def test_composition_equals_sort():
+    keys = skewed_keys(180_001, 99)
+    part, off = hs.hs_msd_partition(dev(keys), 9)
+    cs = hs.hs_sort_chunks(part, off, 8)
+    merged = hs.hs_merge(cs, off, 8)
+    d = dev(keys)
+    hs.hs_sort(d, 9, 8)
+    assert_same(host(merged), host(d), "composition")
+    assert_same(host(d), O.sort(keys, 9, 8), "oracle")
+
+
+def test_sort_on_side_stream_and_graph():
+    keys = rand_keys(77_777, 10**6, 31, np.int32)
+    ref = O.sort(keys, 6, 8)
+    s = torch.cuda.Stream()
+    d = dev(keys)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        hs.hs_sort(d, 6, 8)
+    s.synchronize()
+    assert_same(host(d), ref, "side stream")
+    # whole call captured in a CUDA graph (no host sync inside the call)
+    src = dev(keys)
+    buf = src.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        hs.hs_sort(buf, 6, 8, stream=s)
+    for _ in range(2):
+        buf.copy_(src)
+        g.replay()
+        assert_same(host(buf), ref, "graph replay")
+
+
+# --------------------------------------------------------- full-size configs
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_config_full_bitexact(name):
+    cfg = W.CONFIGS[name]
+    keys = W.generate(name)
+    d = dev(keys)
+    hs.hs_sort(d, cfg.num_digits, cfg.chunks)
+    ref = O.sort(keys, cfg.num_digits, cfg.chunks, openmp=True)
+    assert_same(host(d), ref, name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_config_full_sampled(name):
+    """Full size in bench's launch configuration: partition bit-exact vs the
+    oracle; sort checked on oracle-computed samples (three whole buckets
+    sorted by the oracle's quicksort) plus size-independent invariants
+    (nondecreasing; multiset fingerprint equal to the input's)."""
+    cfg = W.CONFIGS[name]
+    keys = W.generate(name)
+    d = dev(keys)
+    out, off = hs.hs_msd_partition(d, cfg.num_digits)
+    ref_part, ref_off = O.msd_partition(keys, cfg.num_digits)
+    assert_same(host(off), ref_off, "offsets")
+    assert_same(host(out), ref_part.astype(keys.dtype), "partition")
+    del out, ref_part
+    hs.hs_sort(d, cfg.num_digits, cfg.chunks)
+    got = host(d)
+    assert np.all(got[1:] >= got[:-1])
+    assert W.fingerprint(got) == W.fingerprint(keys)
+    for b in (0, 4, 9):
+        lo, hi = int(ref_off[b]), int(ref_off[b + 1])
+        bucket = keys[(np.clip(keys // 10 ** (cfg.num_digits - 1), 0, 9)) == b]
+        assert_same(got[lo:hi], O.quicksort(bucket), f"bucket {b}")
