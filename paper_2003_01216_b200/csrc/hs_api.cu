@@ -110,34 +110,43 @@ void digit_params(int D, hs_dtype_t dt, unsigned long long *div, unsigned long l
     *magic = dt == HS_INT32 ? (0xFFFFFFFFull / d) : (~0ull / d);
 }
 
-// Scratch for one call: [S keys][Ctl][lookback status][co-ranks], one
-// stream-ordered allocation.  Ctl + status are zeroed by one memset.
+// Scratch for one call, one stream-ordered allocation:
+//   [S: n keys][Ctl][K2 lookback status] [K1 tile histograms][K2 tile prefixes][K6 co-ranks]
+// Ctl + status are zeroed by one memset.
 struct Workspace {
     char *base = nullptr;
     void *S = nullptr;
     hs::Ctl *ctl = nullptr;
     unsigned long long *status = nullptr;
+    uint32_t *tile_hist = nullptr;
+    uint32_t *tile_pref = nullptr;
     int *corank = nullptr;
     size_t zero_bytes = 0;
 };
 
-hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t corank_words, cudaStream_t st) {
+hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
+                     cudaStream_t st) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
+    size_t th = round_up(ntiles * 5 * 4, 256);
+    size_t tp = round_up(ntiles * 10 * 4, 256);
     size_t k = round_up(corank_words * 4, 256);
-    size_t total = a + c + z + k;
+    size_t total = a + c + z + th + tp + k;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed: %s", total, cudaGetErrorString(e));
     }
-    w->base = (char *)p;
-    w->S = s_bytes ? w->base : nullptr;
-    w->ctl = (hs::Ctl *)(w->base + a);
-    w->status = (unsigned long long *)(w->base + a + c);
-    w->corank = (int *)(w->base + a + c + z);
+    char *b = (char *)p;
+    w->base = b;
+    w->S = s_bytes ? b : nullptr;
+    w->ctl = (hs::Ctl *)(b + a);
+    w->status = (unsigned long long *)(b + a + c);
+    w->tile_hist = (uint32_t *)(b + a + c + z);
+    w->tile_pref = (uint32_t *)(b + a + c + z + th);
+    w->corank = (int *)(b + a + c + z + th + tp);
     w->zero_bytes = c + z;
     return HS_OK;
 }
@@ -197,7 +206,8 @@ int hs_last_launch_count(void) { return g_launches; }
 
 int hs_tile_keys(hs_dtype_t dtype, int which) {
     if (dtype != HS_INT32 && dtype != HS_INT64) return 0;
-    return hs::tile_keys((int)dtype, which);
+    const int dt = (int)dtype;
+    return which == 0 ? hs::scatter_tile_keys(dt) : which == 1 ? hs::sort_tile_keys(dt) : hs::merge_span(dt);
 }
 
 hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int64_t *bucket_offsets,
@@ -216,21 +226,20 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
 
     const int dt = (int)dtype;
-    const int Tp = hs::tile_keys(dt, 0);
+    const int Tp = hs::scatter_tile_keys(dt);
     const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
     const long long tiles = (n + h + Tp - 1) / Tp;
     unsigned long long div, magic;
     digit_params(num_digits, dtype, &div, &magic);
 
     Workspace ws;
-    if ((s = ws_alloc(&ws, 0, (size_t)tiles * 10, 0, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, stream)) != HS_OK) return s;
     int launches = 0;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
-    HS_TRY_CUDA(hs::launch_histogram(dt, keys, (int)n, h, div, magic, ws.ctl, (long long *)bucket_offsets, -1, 0, sms,
-                                     stream),
-                "K1 histogram");
-    if (n > 0)
-        HS_TRY_CUDA(hs::launch_scatter(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.status, stream), "K3 scatter");
+    HS_TRY_CUDA(hs::launch_partition(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status,
+                                     (long long *)bucket_offsets, -1, 0, 0, sms, true, stream),
+                "K1-K3 partition");
+    launches += (tiles > 0 ? 2 : 0);  // K1, K2, K3 (K1/K3 skipped when n = 0)
     return finish(ws, stream, launches - 1);  // the memset is not one of our kernels
 }
 
@@ -252,7 +261,7 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
 
     const int dt = (int)dtype;
-    const int Tp = hs::tile_keys(dt, 0), T = hs::tile_keys(dt, 1), TM = hs::tile_keys(dt, 2);
+    const int Tp = hs::scatter_tile_keys(dt), T = hs::sort_tile_keys(dt), TM = hs::merge_span(dt);
     const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
     const long long ptiles = (n + h + Tp - 1) / Tp;
     const long long nblocks = (n + TM - 1) / TM;
@@ -260,23 +269,25 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     digit_params(num_digits, dtype, &div, &magic);
 
     Workspace ws;
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)ptiles * 10, (size_t)nblocks + 2, stream)) != HS_OK)
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
+                      (size_t)nblocks + 2, stream)) != HS_OK)
         return s;
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
-    // a1: histogram + bucket offsets + plan (last CTA)
-    HS_TRY_CUDA(hs::launch_histogram(dt, keys, (int)n, h, div, magic, ws.ctl, nullptr, hs::kPlanSort, log2c, sms, stream),
-                "K1 histogram");
-    // a2+a3: stable scatter keys -> S
-    HS_TRY_CUDA(hs::launch_scatter(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.status, stream), "K3 scatter");
+    // a1-a3: tile histograms, lookback prefix (+ offsets + plan), stable scatter keys -> S
+    HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                     ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream),
+                "K1-K3 partition");
+    launches += 2;
     // a5: leaf-tile sort S -> (keys | S) per bucket parity
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, tile_bound(n, chunks_per_bucket, T), stream),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
     for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, lv, (int)n, stream), "K6 merge level");
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, lv, (int)n, sms, stream),
+                    "K6 merge level");
         ++launches;  // partition + merge
     }
     return finish(ws, stream, launches - 1);
@@ -301,18 +312,18 @@ hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtyp
     cudaError_t e = device_setup(&sms);
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
     const int dt = (int)dtype;
-    const int T = hs::tile_keys(dt, 1), TM = hs::tile_keys(dt, 2);
+    const int T = hs::sort_tile_keys(dt), TM = hs::merge_span(dt);
     const long long nblocks = (n + TM - 1) / TM;
 
     Workspace ws;
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanChunks, T, stream), "K4 plan");
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, in, out, ws.S, tile_bound(n, chunks_per_bucket, T), stream), "K5 tile sort");
     const int L = level_bound(n, log2c, T, 1, 0);
     for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, lv, (int)n, stream), "K6 merge level");
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, lv, (int)n, sms, stream), "K6 merge level");
         ++launches;
     }
     return finish(ws, stream, launches);
@@ -337,7 +348,7 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
     cudaError_t e = device_setup(&sms);
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
     const int dt = (int)dtype;
-    const int TM = hs::tile_keys(dt, 2);
+    const int TM = hs::merge_span(dt);
     const long long nblocks = (n + TM - 1) / TM;
     int launches = 0;
     Workspace ws;
@@ -347,7 +358,7 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
         g_err[0] = 0;
         return HS_OK;
     }
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanMerge, 1, stream), "K4 plan");
     const void *src0 = in;
@@ -358,7 +369,7 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
         if (log2c & 1) HS_TRY_CUDA(hs::launch_copy(dt, in, ws.S, n, sms, stream), "K7 copy");
     }
     for (int lv = 0; lv < log2c; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, lv, (int)n, stream), "K6 merge level");
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, lv, (int)n, sms, stream), "K6 merge level");
         ++launches;
     }
     return finish(ws, stream, launches);

@@ -1,7 +1,9 @@
 // hs_launch.h -- internal host-side launch interface between the C ABI
-// (hs_api.cu) and the kernels (hs_kernels.cu).  dt: 0 = int32, 1 = int64.
+// (hs_api.cu) and the kernels (k_partition.cu, k_tilesort.cu, k_merge.cu).
+// dt: 0 = int32, 1 = int64.
 #pragma once
 
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace hs {
@@ -9,17 +11,21 @@ namespace hs {
 struct Ctl;
 struct Plan;
 
-int tile_keys(int dt, int which);  // 0 scatter tile, 1 tile-sort tile, 2 merge CTA span
+int scatter_tile_keys(int dt);  // keys per K1/K3 tile
+int sort_tile_keys(int dt);     // leaf-tile capacity T of K5
+int merge_span(int dt);         // outputs per K6 piece (TM)
+int scan_ctas(long long ntiles);
 
-cudaError_t launch_histogram(int dt, const void *keys, int n, int h, unsigned long long div, unsigned long long magic,
-                             Ctl *ctl, long long *user_off, int plan_mode, int log2c, int num_sms, cudaStream_t st);
-cudaError_t launch_scatter(int dt, const void *keys, void *out, int n, int h, unsigned long long div,
-                           unsigned long long magic, Ctl *ctl, unsigned long long *status, cudaStream_t st);
+// K1 + K2 (+ K3 if do_scatter): partition keys -> out, offsets -> ctl->off (+ user_off), plan if plan_mode >= 0
+cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, unsigned long long div,
+                             unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
+                             unsigned long long *status, long long *user_off, int plan_mode, int log2c,
+                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
                              cudaStream_t st);
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank, int level,
-                               int n, cudaStream_t st);
+                               int n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);
 
 }  // namespace hs
