@@ -6,21 +6,30 @@
 //                          run pair of every bucket at one level
 //   K7  k_copy             in-place hs_merge with an odd number of rounds
 //
-// K6b pipeline (per CTA, one elected producer thread):
-//   produce(piece i+1): geometry -> two 1-D bulk async copies (TMA engine) of
-//                       the A and B slices into stage[(i+1)&1], mbarrier
-//                       completion by byte count
-//   consume(piece i):   sentinels after both slices, per-thread merge-path
-//                       split in shared memory, branch-free serial merge of VT
-//                       outputs (stable-left: ties take A), staging in
-//                       shared memory at the destination's 16-byte phase, one
-//                       1-D bulk async store of the aligned middle + scalar
-//                       head/tail.
+// K6b pipeline (per CTA, warp-specialised):
+//   producer warp: piece geometry -> two 1-D bulk async copies (TMA engine)
+//                  of the A and B slices into a ring of ST stages; full /
+//                  empty mbarriers (full completes on the byte count)
+//   consumer warps: per-thread merge-path split in shared memory,
+//                  branch-free serial merge of VT outputs (stable-left: ties
+//                  take A), staging in shared memory at the
+//                  destination's 16-byte phase, one 1-D bulk async store of the
+//                  aligned middle per piece + scalar head/tail.
 // All data movement of the level is bulk copies; threads only merge.
 #include <cstdint>
 
 #include "hs_device.cuh"
 #include "hs_launch.h"
+
+#ifndef HS_MERGE_NT
+#define HS_MERGE_NT 256
+#endif
+#ifndef HS_MERGE_VT
+#define HS_MERGE_VT 16
+#endif
+#ifndef HS_MERGE_ST
+#define HS_MERGE_ST 3
+#endif
 
 namespace hs {
 
@@ -28,11 +37,11 @@ template <typename K>
 struct MGeo;
 template <>
 struct MGeo<int32_t> {
-    static constexpr int kNT = 256, kVT = 16;  // 4096 outputs per piece
+    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT, kST = HS_MERGE_ST;  // default 256 x 16, 3 stages
 };
 template <>
 struct MGeo<int64_t> {
-    static constexpr int kNT = 256, kVT = 8;  // 2048 outputs per piece
+    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT / 2, kST = HS_MERGE_ST;
 };
 
 template <typename K>
@@ -85,148 +94,199 @@ template <typename K>
 struct Piece {
     long long x;  // first output position
     K *dst;
-    int len, na, nb;
-    int offA, offB;  // element offsets of the A / B slices inside the stage
+    int len, na, nb;  // len < 0: no more pieces
+    int offA, offB;   // element offsets of the A / B slices inside the stage
 };
 
-template <typename K, int NT, int VT>
+template <typename K, int NC, int VT, int ST>
 struct MergeSmem {
-    static constexpr int TM = NT * VT;
+    static constexpr int TM = NC * VT;
     static constexpr int E = 16 / sizeof(K);
-    // A superset (<= TM_A + 2E) | VT sentinels | pad to 16 B | B superset | VT sentinels
-    static constexpr int SLOT = ((TM + 4 * E + 2 * VT + 2 * E) + E - 1) / E * E;
+    // A superset (<= na + 2E) | pad to 16 B | B superset (<= nb + 2E)
+    // (+VT: exhausted-run indices may run up to VT past a slice; reads are masked)
+    static constexpr int SLOT = (TM + 6 * E + VT + E - 1) / E * E;
     static constexpr int OUT = TM + E;
-    static constexpr size_t bytes() { return (size_t)(2 * SLOT + OUT) * sizeof(K); }
+    static constexpr size_t bytes() { return (size_t)(ST * SLOT + 2 * OUT) * sizeof(K); }
 };
 
-template <typename K, int NT, int VT>
-__global__ void __launch_bounds__(NT) k_merge_level(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
-                                                    const int *__restrict__ corank, int level, int n, int nblocks) {
-    using SM = MergeSmem<K, NT, VT>;
-    constexpr int TM = SM::TM, E = SM::E, SLOT = SM::SLOT;
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Merge-path split of output diag between A[0..na) and B[0..nb) (stable-left).
+template <typename K>
+__device__ __forceinline__ int merge_path(const K *A, int na, const K *B, int nb, int diag) {
+    int l = diag - nb > 0 ? diag - nb : 0;
+    int r = diag < na ? diag : na;
+    while (l < r) {
+        const int mid = (l + r) >> 1;
+        if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
+        else r = mid;
+    }
+    return l;
+}
+
+// Warp-specialised: warps 0..NC/32-1 merge, the last warp produces.
+//   producer: piece geometry -> stage ring (ST slots, full/empty mbarriers),
+//             A and B slices fetched by 1-D bulk async copies.
+//   consumers: merge-path split + branch-free serial merge of VT outputs per
+//             thread, staging (double-buffered) at the destination's 16-byte
+//             phase, one bulk async store of the aligned middle per piece.
+template <typename K, int NC, int VT, int ST>
+__global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
+                                                         const int *__restrict__ corank, int level, int n,
+                                                         int nblocks) {
+    using SM = MergeSmem<K, NC, VT, ST>;
+    constexpr int TM = SM::TM, E = SM::E, SLOT = SM::SLOT, OUT = SM::OUT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     K *const stage0 = reinterpret_cast<K *>(smem_raw);
-    K *const sOut = stage0 + 2 * SLOT;
-    __shared__ __align__(8) uint64_t mbar[2];
+    K *const out0 = stage0 + ST * SLOT;
+    __shared__ __align__(8) uint64_t full[ST];
+    __shared__ __align__(8) uint64_t empty[ST];
     __shared__ Plan P;
-    __shared__ Piece<K> pc[2];
-    __shared__ int s_more[2];
+    __shared__ Piece<K> pc[ST];
     const int tid = threadIdx.x;
     const K kMax = KeyTraits<K>::kMax;
 
     load_plan_m(P, plan_g);
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int i = 0; i < ST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NC / 32);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    // producer state (meaningful in thread 0 only)
-    int blk = blockIdx.x;
-    long long px = (long long)blk * TM;
-
-    // Find the next piece after (blk, px), issue its loads into `slot`.
-    auto produce = [&](int slot) -> int {
-        while (blk < nblocks) {
-            const long long P0 = (long long)blk * TM;
-            const long long P1 = P0 + TM < n ? P0 + TM : (long long)n;
-            if (px >= P1) {
-                blk += gridDim.x;
-                px = (long long)blk * TM;
-                continue;
-            }
-            const int b = bucket_of(P, px);
-            if (level >= P.L[b]) {
-                px = P.off[b + 1];
-                continue;
-            }
-            const PairGeom g = pair_of(P, b, leaf_of(P, b, px), level);
-            const long long e = P1 < g.b_hi ? P1 : g.b_hi;
-            // px is either a pair start or the block start P0 (whose co-rank K6a stored)
-            const long long ax = (px == g.a_lo) ? g.a_lo : (long long)corank[blk];
-            const long long ae = (e == g.b_hi) ? g.b_lo : (long long)corank[blk + 1];
-            const long long bx = g.b_lo + (px - ax);
-            const long long be = g.b_lo + (e - ae);
-            const K *src = (level == 0 && src0) ? src0 : level_src(P, b, level, F, S);
+    if (tid >= NC) {
+        // ------------------------------------------------------ producer
+        if (tid != NC) return;
+        int blk = blockIdx.x;
+        long long px = (long long)blk * TM;
+        for (int it = 0;; ++it) {
+            const int slot = it % ST;
+            mbar_wait(&empty[slot], ((it / ST) & 1) ^ 1);
             Piece<K> q;
-            q.x = px;
-            q.dst = level_dst(P, b, level, F, S);
-            q.na = (int)(ae - ax);
-            q.nb = (int)(be - bx);
-            q.len = (int)(e - px);
-            const uintptr_t ga0 = (uintptr_t)(src + ax) & ~(uintptr_t)15;
-            const uintptr_t ga1 = ((uintptr_t)(src + ae) + 15) & ~(uintptr_t)15;
-            const uintptr_t gb0 = (uintptr_t)(src + bx) & ~(uintptr_t)15;
-            const uintptr_t gb1 = ((uintptr_t)(src + be) + 15) & ~(uintptr_t)15;
-            const uint32_t bytesA = q.na > 0 ? (uint32_t)(ga1 - ga0) : 0u;
-            const uint32_t bytesB = q.nb > 0 ? (uint32_t)(gb1 - gb0) : 0u;
-            q.offA = (int)(((uintptr_t)(src + ax) - ga0) / sizeof(K));
-            // B's superset starts at the first 16-byte boundary past A's slice + VT sentinels
-            const int bstart = ((q.offA + q.na + VT) + E - 1) / E * E;
-            const int bstart2 = bstart * (int)sizeof(K) >= (int)bytesA ? bstart : (int)(bytesA / sizeof(K));
-            q.offB = bstart2 + (int)(((uintptr_t)(src + bx) - gb0) / sizeof(K));
-            K *st = stage0 + slot * SLOT;
-            fence_proxy_async_smem();  // prior generic reads of this slot precede the async writes
-            mbar_arrive_expect_tx(&mbar[slot], bytesA + bytesB);
-            if (bytesA) bulk_g2s(st, (const void *)ga0, bytesA, &mbar[slot]);
-            if (bytesB) bulk_g2s(st + bstart2, (const void *)gb0, bytesB, &mbar[slot]);
-            pc[slot] = q;
-            px = e;
-            return 1;
+            q.len = -1;
+            while (blk < nblocks) {
+                const long long P0 = (long long)blk * TM;
+                const long long P1 = P0 + TM < n ? P0 + TM : (long long)n;
+                if (px >= P1) {
+                    blk += gridDim.x;
+                    px = (long long)blk * TM;
+                    continue;
+                }
+                const int b = bucket_of(P, px);
+                if (level >= P.L[b]) {
+                    px = P.off[b + 1];
+                    continue;
+                }
+                const PairGeom g = pair_of(P, b, leaf_of(P, b, px), level);
+                const long long e = P1 < g.b_hi ? P1 : g.b_hi;
+                // px is either a pair start or the block start P0 (co-rank from K6a)
+                const long long ax = (px == g.a_lo) ? g.a_lo : (long long)corank[blk];
+                const long long ae = (e == g.b_hi) ? g.b_lo : (long long)corank[blk + 1];
+                const long long bx = g.b_lo + (px - ax);
+                const long long be = g.b_lo + (e - ae);
+                const K *src = (level == 0 && src0) ? src0 : level_src(P, b, level, F, S);
+                q.x = px;
+                q.dst = level_dst(P, b, level, F, S);
+                q.na = (int)(ae - ax);
+                q.nb = (int)(be - bx);
+                q.len = (int)(e - px);
+                const uintptr_t ga0 = (uintptr_t)(src + ax) & ~(uintptr_t)15;
+                const uintptr_t ga1 = ((uintptr_t)(src + ae) + 15) & ~(uintptr_t)15;
+                const uintptr_t gb0 = (uintptr_t)(src + bx) & ~(uintptr_t)15;
+                const uintptr_t gb1 = ((uintptr_t)(src + be) + 15) & ~(uintptr_t)15;
+                const uint32_t bytesA = q.na > 0 ? (uint32_t)(ga1 - ga0) : 0u;
+                const uint32_t bytesB = q.nb > 0 ? (uint32_t)(gb1 - gb0) : 0u;
+                q.offA = (int)(((uintptr_t)(src + ax) - ga0) / sizeof(K));
+                const int bstart = (int)(bytesA / sizeof(K));  // multiple of E
+                q.offB = bstart + (int)(((uintptr_t)(src + bx) - gb0) / sizeof(K));
+                K *st = stage0 + slot * SLOT;
+                pc[slot] = q;
+                mbar_arrive_expect_tx(&full[slot], bytesA + bytesB);
+                if (bytesA) bulk_g2s(st, (const void *)ga0, bytesA, &full[slot]);
+                if (bytesB) bulk_g2s(st + bstart, (const void *)gb0, bytesB, &full[slot]);
+                px = e;
+                break;
+            }
+            if (q.len < 0) {
+                pc[slot] = q;
+                mbar_arrive_expect_tx(&full[slot], 0);
+                return;
+            }
         }
-        return 0;
-    };
+    }
 
-    if (tid == 0) s_more[0] = produce(0);
-    __syncthreads();
-    uint32_t phases = 0u;  // bit s = parity of stage s's mbarrier
-    int cur = 0;
-    while (s_more[cur]) {
-        if (tid == 0) s_more[cur ^ 1] = produce(cur ^ 1);
-        mbar_wait(&mbar[cur], (phases >> cur) & 1u);
-        phases ^= 1u << cur;
-        const Piece<K> q = pc[cur];
-        K *const sb = stage0 + cur * SLOT;
-        // VT sentinels after each slice (overwrites superset spill-over)
-        if (tid < VT) sb[q.offA + q.na + tid] = kMax;
-        else if (tid < 2 * VT) sb[q.offB + q.nb + tid - VT] = kMax;
-        __syncthreads();
-
+    // ---------------------------------------------------------- consumers
+    const int lane = tid & 31;
+    for (int it = 0;; ++it) {
+        const int slot = it % ST;
+        mbar_wait(&full[slot], (it / ST) & 1);
+        const Piece<K> q = pc[slot];
+        if (q.len < 0) break;
+        const K *sb = stage0 + slot * SLOT;
+        const K *A = sb + q.offA;
+        const K *B = sb + q.offB;
+        const int na = q.na, nb = q.nb;
         // staging position p holds output p - sh; sh = destination's 16-byte phase
         const int sh = (int)(((uintptr_t)(q.dst + q.x) & 15) / sizeof(K));
         const int p_lo = tid * VT > sh ? tid * VT : sh;
         const int diag = p_lo - sh;
         K v[VT];
         if (diag < q.len) {
-            int l = diag - q.nb > 0 ? diag - q.nb : 0;
-            int r = diag < q.na ? diag : q.na;
-            const K *A = sb + q.offA;
-            const K *B = sb + q.offB;
-            while (l < r) {
-                const int mid = (l + r) >> 1;
-                if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
-                else r = mid;
-            }
-            int ai = q.offA + l, bi = q.offB + diag - l;
-            K a = sb[ai], b = sb[bi];
+            const int a0 = merge_path(A, na, B, nb, diag);
+            // indices into the stage; an exhausted run reads as kMax (an
+            // exhausted A only "wins" a tie against a real kMax in B, and then
+            // emits the same value), so the loop needs no bounds branches
+            const int a_end = q.offA + na, b_end = q.offB + nb;
+            int ai = q.offA + a0, bi = q.offB + diag - a0;
+            K x = ai < a_end ? sb[ai] : kMax;
+            K y = bi < b_end ? sb[bi] : kMax;
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
-                const bool p = a <= b;
-                v[k] = p ? a : b;
+                const bool p = x <= y;
+                v[k] = p ? x : y;
                 if (k + 1 < VT) {
                     const int nx = (p ? ai : bi) + 1;
+                    const int lim = p ? a_end : b_end;
                     const K t = sb[nx];
+                    const K tv = nx < lim ? t : kMax;
                     ai = p ? nx : ai;
                     bi = p ? bi : nx;
-                    a = p ? t : a;
-                    b = p ? b : t;
+                    x = p ? tv : x;
+                    y = p ? y : tv;
                 }
             }
         }
-        // the previous piece's bulk store must have finished reading sOut
-        if (tid == 0) bulk_wait_read0();
-        __syncthreads();
+        // overhang: with sh > 0 a full piece spans up to E-1 positions past NC*VT
+        const int over = sh + q.len - NC * VT;
+        K vx[E];
+        if (over > 0 && tid == NC - 1) {
+            const int dx = NC * VT - sh;
+            int ai = merge_path(A, na, B, nb, dx), bi = dx - ai;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const K x = ai < na ? A[ai] : kMax;
+                const K y = bi < nb ? B[bi] : kMax;
+                const bool p = (bi >= nb) || (ai < na && x <= y);
+                vx[k] = p ? x : y;
+                ai += p ? 1 : 0;
+                bi += p ? 0 : 1;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the stage
+
+        K *sOut = out0 + (it & 1) * OUT;
+        if (tid == 0) bulk_wait_read1();  // the store two pieces ago has read sOut
+        consumer_bar(NC);
         const int end = sh + q.len;
         if (diag < q.len) {
             if (tid * VT >= sh && (tid + 1) * VT <= end) {
@@ -244,29 +304,31 @@ __global__ void __launch_bounds__(NT) k_merge_level(const Plan *__restrict__ pla
                 }
             }
         }
-        fence_proxy_async_smem();  // make the staged outputs visible to the bulk store
-        __syncthreads();
-        const int m0 = sh == 0 ? 0 : E;       // first 16-byte aligned staging position
-        const int m1 = end / E * E;            // last one
-        K *const g = q.dst + q.x - sh;        // staging position p <-> g[p]
+        if (over > 0 && tid == NC - 1) {
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                if (k < over) sOut[NC * VT + k] = vx[k];
+        }
+        fence_proxy_async_smem();  // staged outputs -> visible to the bulk store
+        consumer_bar(NC);
+        const int m0 = sh == 0 ? 0 : E;  // first 16-byte aligned staging position
+        const int m1 = end / E * E;      // last one
+        K *const g = q.dst + q.x - sh;   // staging position p <-> g[p]
         if (m1 > m0) {
-            if (tid == 0) {
-                bulk_s2g(g + m0, sOut + m0, (uint32_t)((m1 - m0) * sizeof(K)));
-                bulk_commit();
-            }
+            if (tid == 0) bulk_s2g(g + m0, sOut + m0, (uint32_t)((m1 - m0) * sizeof(K)));
             if (tid < E) {
                 const int p = sh + tid;  // head
                 if (p < m0 && p < end) g[p] = sOut[p];
             } else if (tid < 2 * E) {
                 const int p = m1 + tid - E;  // tail
-                if (p < end && p >= m0) g[p] = sOut[p];
+                if (p < end) g[p] = sOut[p];
             }
         } else {
-            for (int p = sh + tid; p < end; p += NT) g[p] = sOut[p];
+            for (int p = sh + tid; p < end; p += NC) g[p] = sOut[p];
         }
-        cur ^= 1;
+        if (tid == 0) bulk_commit();  // one group per piece (possibly empty)
     }
-    if (tid == 0) bulk_wait_read0();
+    if (tid == 0) bulk_wait0();
 }
 
 // =================================================================== K7
@@ -286,19 +348,21 @@ template <typename K>
 cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void *src0, int *corank, int level, int n,
                                  int num_sms, cudaStream_t st) {
     using G = MGeo<K>;
-    using SM = MergeSmem<K, G::kNT, G::kVT>;
+    using SM = MergeSmem<K, G::kNT, G::kVT, G::kST>;
     constexpr int TM = SM::TM;
-    static bool configured = false;  // per process; attribute is per function
+    auto kern = k_merge_level<K, G::kNT, G::kVT, G::kST>;
+    static int configured_dev = -1;
     static int per_sm = 1;
-    auto kern = k_merge_level<K, G::kNT, G::kVT>;
-    if (!configured) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::bytes());
         if (e != cudaSuccess) return e;
         int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kNT, SM::bytes());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kNT + 32, SM::bytes());
         if (e != cudaSuccess) return e;
         per_sm = occ > 0 ? occ : 1;
-        configured = true;
+        configured_dev = dev;
     }
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
@@ -309,7 +373,8 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     if (e != cudaSuccess) return e;
     long long grid = (long long)per_sm * num_sms;
     if (grid > nblocks) grid = nblocks;
-    kern<<<(unsigned)grid, G::kNT, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank, level, n, nblocks);
+    kern<<<(unsigned)grid, G::kNT + 32, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank, level, n,
+                                                           nblocks);
     return cudaGetLastError();
 }
 

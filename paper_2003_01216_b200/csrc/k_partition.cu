@@ -23,6 +23,13 @@
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
+#ifndef HS_SCAT_NT
+#define HS_SCAT_NT 256
+#endif
+#ifndef HS_SCAT_VT
+#define HS_SCAT_VT 16
+#endif
+
 namespace hs {
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
@@ -33,11 +40,11 @@ template <typename K>
 struct PGeo;
 template <>
 struct PGeo<int32_t> {
-    static constexpr int kScatNT = 256, kScatVT = 16;  // 4096 keys per tile
+    static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT;  // default 256 x 16 = 4096 keys per tile
 };
 template <>
 struct PGeo<int64_t> {
-    static constexpr int kScatNT = 256, kScatVT = 8;  // 2048 keys per tile
+    static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT / 2;
 };
 constexpr int kHistWarps = 8;
 constexpr int kScanNT = 256, kScanIPT = 8;  // 2048 tile histograms per K2 CTA
@@ -248,58 +255,46 @@ __global__ void __launch_bounds__(kScanNT) k_tile_scan(const uint32_t *__restric
 
 // =================================================================== K3
 template <typename K, int NT, int VT>
-__global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *__restrict__ out, int n, int h,
-                                                DigitParams<K> dp, const Ctl *__restrict__ ctl,
-                                                const uint32_t *__restrict__ tile_pref) {
-    constexpr int T = NT * VT;
+struct ScatSmem {
+    static constexpr int T = NT * VT;
+    static constexpr size_t bytes() { return (size_t)3 * T * sizeof(K) + T; }  // 2 stages + out + digits
+};
+
+// Rank + re-stage one tile held in `stage` (blocked: thread tid owns slots
+// tid*VT ..).  FULL: every slot is a key (interior tile) -> no validity tests.
+template <typename K, int NT, int VT, bool FULL>
+__device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__restrict__ sOut, uint8_t *sDig,
+                                             K *__restrict__ out, int jlo, int jhi, int tile, const DigitParams<K> &dp,
+                                             const Ctl *__restrict__ ctl, const uint32_t *__restrict__ tile_pref,
+                                             unsigned (*s_wtot)[5], int *s_dstart, int *s_delta) {
     constexpr int E = 16 / sizeof(K);
     constexpr int NW = NT / 32;
     constexpr int NMETA = VT / 4 > 0 ? VT / 4 : 1;
-    static_assert(VT <= 16 && T <= 16384, "packing limits");
-    __shared__ K s[T + T / 32];
-    __shared__ uint8_t s_dig[T];
-    __shared__ unsigned s_wtot[NW][5];
-    __shared__ int s_dstart[10];
-    __shared__ long long s_delta[10];
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tile = blockIdx.x;
-    const long long v0 = (long long)tile * T - h;
-    const int jlo = v0 < 0 ? (int)(-v0) : 0;
-    const int jhi = (int)((long long)n - v0 < T ? (long long)n - v0 : (long long)T);
 
-    // load the tile (coalesced 128-bit) into padded shared memory
-#pragma unroll
-    for (int r = 0; r < T / E / NT; ++r) {
-        const int j0 = (r * NT + tid) * E;
-        K vals[E];
-        if (j0 >= jlo && j0 + E <= jhi) {
-            int4 q = ld_stream_v4(keys + (v0 + j0));
-            memcpy(vals, &q, 16);
-        } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) vals[e] = (j0 + e >= jlo && j0 + e < jhi) ? keys[v0 + j0 + e] : K(0);
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) s[pad_idx(j0 + e)] = vals[e];
-    }
-    __syncthreads();
-
-    // rank: thread owns slots tid*VT .. (input order); 6-bit packed counters
-    K key[VT];
     unsigned meta[NMETA];
 #pragma unroll
     for (int i = 0; i < NMETA; ++i) meta[i] = 0;
     unsigned long long cnt = 0;
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int j = tid * VT + k;
-        key[k] = s[pad_idx(j)];
-        const bool valid = (j >= jlo) && (j < jhi);
-        const int d = valid ? msd_digit(key[k], dp) : 10;  // field 10 = "not a key"
-        const unsigned r = (unsigned)(cnt >> (6 * d)) & 63u;
-        cnt += 1ull << (6 * d);
-        meta[k >> 2] |= ((unsigned)d | (r << 4)) << (8 * (k & 3));
+    for (int k0 = 0; k0 < VT; k0 += E) {
+        K kv[E];
+        const int4 q = *reinterpret_cast<const int4 *>(stage + tid * VT + k0);
+        memcpy(kv, &q, 16);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int k = k0 + e;
+            int d;
+            if (FULL) {
+                d = msd_digit(kv[e], dp);
+            } else {
+                const int j = tid * VT + k;
+                d = (j >= jlo && j < jhi) ? msd_digit(kv[e], dp) : 10;  // field 10 = "not a key"
+            }
+            const unsigned r = (unsigned)(cnt >> (6 * d)) & 63u;
+            cnt += 1ull << (6 * d);
+            meta[k >> 2] |= ((unsigned)d | (r << 4)) << (8 * (k & 3));
+        }
     }
     // block exclusive scan of per-thread digit counts (5 words x 2 16-bit fields)
     unsigned own[5], w[5];
@@ -312,7 +307,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
     for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
         for (int i = 0; i < 5; ++i) {
-            unsigned t = __shfl_up_sync(0xffffffffu, w[i], o);
+            const unsigned t = __shfl_up_sync(0xffffffffu, w[i], o);
             if (lane >= o) w[i] += t;
         }
     }
@@ -332,7 +327,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
         for (int o = 1; o < NW; o <<= 1) {
 #pragma unroll
             for (int i = 0; i < 5; ++i) {
-                unsigned u = __shfl_up_sync(0xffffffffu, t[i], o);
+                const unsigned u = __shfl_up_sync(0xffffffffu, t[i], o);
                 if (lane >= o) t[i] += u;
             }
         }
@@ -352,7 +347,8 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
                 if (e < lane) dstart += f;
             }
             s_dstart[lane] = (int)dstart;
-            s_delta[lane] = ctl->off[lane] + (long long)tile_pref[(size_t)tile * 10 + lane] - (long long)dstart;
+            // global position of tile-local slot j of digit d = delta[d] + j (< 2^31)
+            s_delta[lane] = (int)(ctl->off[lane] + (long long)tile_pref[(size_t)tile * 10 + lane] - (long long)dstart);
         }
     }
     __syncthreads();
@@ -363,21 +359,85 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
     for (int i = 0; i < 5; ++i)
         base[i] = s_wtot[warp][i] + (w[i] - own[i]) + ((unsigned)s_dstart[2 * i] | ((unsigned)s_dstart[2 * i + 1] << 16));
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const unsigned m = (meta[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-        const unsigned d = m & 15u, r = m >> 4;
-        if (d < 10) {
-            const unsigned wsel = d < 2 ? base[0] : d < 4 ? base[1] : d < 6 ? base[2] : d < 8 ? base[3] : base[4];
-            const int pos = (int)((wsel >> ((d & 1u) * 16)) & 0xFFFFu) + (int)r;
-            s[pad_idx(pos)] = key[k];
-            s_dig[pos] = (uint8_t)d;
+    for (int k0 = 0; k0 < VT; k0 += E) {
+        K kv[E];
+        const int4 q = *reinterpret_cast<const int4 *>(stage + tid * VT + k0);
+        memcpy(kv, &q, 16);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int k = k0 + e;
+            const unsigned m = (meta[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+            const unsigned d = m & 15u, r = m >> 4;
+            if (FULL || d < 10) {
+                const unsigned wsel = d < 2 ? base[0] : d < 4 ? base[1] : d < 6 ? base[2] : d < 8 ? base[3] : base[4];
+                const int pos = (int)((wsel >> ((d & 1u) * 16)) & 0xFFFFu) + (int)r;
+                sOut[pos] = kv[e];
+                sDig[pos] = (uint8_t)d;
+            }
         }
     }
     __syncthreads();
 
     // ten coalesced runs
     const int nvalid = jhi - jlo;
-    for (int j = tid; j < nvalid; j += NT) out[s_delta[s_dig[j]] + j] = s[pad_idx(j)];
+    for (int j = tid; j < nvalid; j += NT) out[s_delta[sDig[j]] + j] = sOut[j];
+}
+
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the next
+// tile is prefetched by one 1-D bulk async copy into the other stage while
+// the current one is ranked and scattered.
+template <typename K, int NT, int VT>
+__global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *__restrict__ out, int n, int h,
+                                                DigitParams<K> dp, const Ctl *__restrict__ ctl,
+                                                const uint32_t *__restrict__ tile_pref, int ntiles) {
+    constexpr int T = NT * VT;
+    constexpr int NW = NT / 32;
+    static_assert(VT <= 16 && T <= 16384, "packing limits");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    K *const stage0 = reinterpret_cast<K *>(smem_raw);
+    K *const sOut = stage0 + 2 * T;
+    uint8_t *const sDig = reinterpret_cast<uint8_t *>(sOut + T);
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ unsigned s_wtot[NW][5];
+    __shared__ int s_dstart[10];
+    __shared__ int s_delta[10];
+    const int tid = threadIdx.x;
+
+    // virtual tile t covers [t*T - h, (t+1)*T - h): 16-byte aligned in memory
+    auto issue = [&](int t, int slot) {
+        const long long v0 = (long long)t * T - h;
+        const long long vend = v0 + T < n ? v0 + T : (long long)n;
+        const uintptr_t g0 = (uintptr_t)(keys + v0);
+        const uintptr_t g1 = ((uintptr_t)(keys + vend) + 15) & ~(uintptr_t)15;
+        const uint32_t bytes = (uint32_t)(g1 - g0);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&mbar[slot], bytes);
+        bulk_g2s(stage0 + slot * T, (const void *)g0, bytes, &mbar[slot]);
+    };
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+        if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    }
+    __syncthreads();
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int slot = it & 1;
+        mbar_wait(&mbar[slot], (it >> 1) & 1);
+        if (tid == 0 && t + (int)gridDim.x < ntiles) issue(t + gridDim.x, slot ^ 1);
+        const long long v0 = (long long)t * T - h;
+        const int jlo = v0 < 0 ? (int)(-v0) : 0;
+        const int jhi = (int)((long long)n - v0 < T ? (long long)n - v0 : (long long)T);
+        const K *stage = stage0 + slot * T;
+        if (jlo == 0 && jhi == T)
+            scatter_tile<K, NT, VT, true>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
+                                          s_delta);
+        else
+            scatter_tile<K, NT, VT, false>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
+                                           s_delta);
+        __syncthreads();  // stage / sOut / tables are reused next iteration
+    }
 }
 
 // =============================================================== launchers
@@ -410,8 +470,25 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
                                            sort_tile_keys);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
-    k_scatter<K, G::kScatNT, G::kScatVT><<<(unsigned)ntiles, G::kScatNT, 0, st>>>((const K *)keys, (K *)out, n, h, dp,
-                                                                                  ctl, tile_pref);
+    using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
+    auto kern = k_scatter<K, G::kScatNT, G::kScatVT>;
+    static int configured_dev = -1;
+    static int per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::bytes());
+        if (e != cudaSuccess) return e;
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kScatNT, SS::bytes());
+        if (e != cudaSuccess) return e;
+        per_sm = occ > 0 ? occ : 1;
+        configured_dev = dev;
+    }
+    long long grid = (long long)per_sm * num_sms;
+    if (grid > ntiles) grid = ntiles;
+    kern<<<(unsigned)grid, G::kScatNT, SS::bytes(), st>>>((const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
+                                                          (int)ntiles);
     return cudaGetLastError();
 }
 

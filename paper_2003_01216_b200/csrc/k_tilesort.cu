@@ -6,15 +6,39 @@
 //
 // The rest of a5 (in-chunk merge levels) and a6 are in k_merge.cu; a1-a3 in
 // k_partition.cu.  Design notes and rooflines: DESIGN.md §5.
+//
+// K5 replaces the paper's per-thread sequential quicksort (Fig 1c, P:50,
+// P:62) -- a data-dependent, branchy, serial algorithm that maps badly onto
+// SIMT lanes -- by the GPU shape of the same "sort the partitions, then merge
+// sorted lists pairwise" idea its parallel sorts are built from:
+//   1. each thread sorts VT keys in registers (Batcher odd-even network,
+//      compile-time register indices, no branches);
+//   2. log2(T/VT) bitonic merge passes: strides inside a warp use warp
+//      shuffles, strides across warps exchange through shared memory.
+// Keys-only data makes the sorted tile unique, so the (unstable) network
+// order is unobservable.  The tile is padded to a power of two with the
+// dtype maximum; pads sort to the end and are never stored (they equal any
+// real maximum key, so the stored prefix is the same multiset).
 #include <cstdint>
-#include <cstring>
 
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
+#ifndef HS_SORT_NT
+#define HS_SORT_NT 256
+#endif
+#ifndef HS_SORT_VT
+#define HS_SORT_VT 32
+#endif
+#ifndef HS_SORT_NT64
+#define HS_SORT_NT64 256
+#endif
+#ifndef HS_SORT_VT64
+#define HS_SORT_VT64 16
+#endif
+
 namespace hs {
 
-// Copy the plan into shared memory (one word per thread).
 __device__ __forceinline__ void load_plan(Plan &dst, const Plan *src) {
     static_assert(sizeof(Plan) % 4 == 0, "plan size");
     constexpr int W = sizeof(Plan) / 4;
@@ -33,17 +57,134 @@ __global__ void k_plan(const long long *__restrict__ user_off, Ctl *ctl, int log
 }
 
 // =================================================================== K5
-// In-shared-memory sort of one leaf tile (a5).  Each thread sorts VT keys
-// in registers with a Batcher odd-even network, then log2(T/VT) merge
-// passes in shared memory: every thread finds its merge-path split by binary
-// search and merges VT outputs serially (stable-left).  Padding with the
-// dtype max makes every tile a full power of two; pads sort to the end and
-// are never stored (they are indistinguishable from real max keys).
-// The tile is written to the buffer where its bucket's level 0 reads.
+// Bitonic tile sort.  Logical element e = t*VT + k lives in register k of
+// thread t.  Sorting runs of width W into runs of 2W ("pass W") is one
+// bitonic merge: a mirror stage (e <-> the mirror of e inside its 2W block,
+// lower half keeps the min) followed by half-cleaner stages of stride
+// W/2 .. 1 (lower index keeps the min).  A stride of S elements is
+//   S <  VT        : inside a thread  -> compare-exchange of two registers
+//   S >= VT, lanes : inside a warp    -> __shfl_xor_sync + predicated min/max
+//   S >= 32*VT     : across warps     -> exchange through shared memory
+// No stage depends on the data, so there are no searches and no
+// data-dependent shared-memory addresses.
+template <typename K>
+__device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
+template <typename K>
+__device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
+
+template <typename K>
+__device__ __forceinline__ K shfl_xor_k(K v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// Half-cleaner stages with stride < VT (registers only).
+template <typename K, int VT>
+__device__ __forceinline__ void intra_stages(K (&v)[VT]) {
+#pragma unroll
+    for (int sd = VT / 2; sd >= 1; sd >>= 1) {
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {
+            if ((k & sd) == 0) {
+                const K a = v[k], b = v[k + sd];
+                v[k] = kmin(a, b);
+                v[k + sd] = kmax(a, b);
+            }
+        }
+    }
+}
+
+// Cross-warp exchange through shared memory (register-major layout
+// sm[k*NT + t]: conflict-free).  partner thread pt, partner register
+// index pk(k) = MIRROR ? VT-1-k : k.
+template <typename K, int NT, int VT, bool MIRROR>
+__device__ __forceinline__ void smem_stage(K *sm, int tid, int pt, bool keep_min, K (&v)[VT]) {
+#pragma unroll
+    for (int k = 0; k < VT; ++k) sm[k * NT + tid] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+        const K o = sm[(MIRROR ? VT - 1 - k : k) * NT + pt];
+        v[k] = keep_min ? kmin(v[k], o) : kmax(v[k], o);
+    }
+    __syncthreads();
+}
+
+// Sort a thread's VT registers ascending: bitonic network with constant
+// register indices (mirror stage + half-cleaners per block size).
+template <typename K, int VT>
+__device__ __forceinline__ void reg_sort(K (&v)[VT]) {
+#pragma unroll
+    for (int size = 2; size <= VT; size <<= 1) {
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {
+            const int base = k & ~(size - 1), off = k - base;
+            if (off < size / 2) {
+                const int m = base + size - 1 - off;
+                const K a = v[k], b = v[m];
+                v[k] = kmin(a, b);
+                v[m] = kmax(a, b);
+            }
+        }
+#pragma unroll
+        for (int sd = size / 4; sd >= 1; sd >>= 1) {
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                if ((k & sd) == 0 && ((k & (size - 1)) + sd) < size) {
+                    const K a = v[k], b = v[k + sd];
+                    v[k] = kmin(a, b);
+                    v[k + sd] = kmax(a, b);
+                }
+            }
+        }
+    }
+}
+
+// One bitonic merge pass turning runs of width W = VT*R into runs of 2W.
+template <typename K, int NT, int VT, int R>
+__device__ __forceinline__ void bitonic_pass(K *sm, int tid, K (&v)[VT]) {
+    const int lane = tid & 31;
+    // mirror stage: thread u (within its 2R-thread block) <-> 2R-1-u, register k <-> VT-1-k
+    const bool lower = (tid & R) == 0;
+    if constexpr (2 * R <= 32) {
+#pragma unroll
+        for (int k = 0; k < VT / 2; ++k) {
+            const K o1 = __shfl_xor_sync(0xffffffffu, v[VT - 1 - k], 2 * R - 1);
+            const K o2 = __shfl_xor_sync(0xffffffffu, v[k], 2 * R - 1);
+            v[k] = lower ? kmin(v[k], o1) : kmax(v[k], o1);
+            v[VT - 1 - k] = lower ? kmin(v[VT - 1 - k], o2) : kmax(v[VT - 1 - k], o2);
+        }
+    } else {
+        smem_stage<K, NT, VT, true>(sm, tid, tid ^ (2 * R - 1), lower, v);
+    }
+    // half-cleaners across threads: thread distance R/2 .. 1
+#pragma unroll
+    for (int d = R / 2; d >= 1; d >>= 1) {
+        const bool lo = (tid & d) == 0;
+        if (d >= 32) {
+            smem_stage<K, NT, VT, false>(sm, tid, tid ^ d, lo, v);
+        } else {
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                const K o = __shfl_xor_sync(0xffffffffu, v[k], d);
+                v[k] = lo ? kmin(v[k], o) : kmax(v[k], o);
+            }
+        }
+    }
+    (void)lane;
+    intra_stages<K, VT>(v);
+}
+
+template <typename K, int NT, int VT, int R>
+__device__ __forceinline__ void bitonic_passes(K *sm, int tid, K (&v)[VT]) {
+    if constexpr (R < NT) {
+        bitonic_pass<K, NT, VT, R>(sm, tid, v);
+        bitonic_passes<K, NT, VT, 2 * R>(sm, tid, v);
+    }
+}
+
 template <typename K, int NT, int VT>
 __global__ void __launch_bounds__(NT) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S) {
     constexpr int T = NT * VT;
-    __shared__ K s[T + T / 32];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K *const sm = reinterpret_cast<K *>(smem_raw);
     __shared__ Plan P;
     const int tid = threadIdx.x;
     load_plan(P, plan_g);
@@ -56,57 +197,30 @@ __global__ void __launch_bounds__(NT) k_tile_sort(const Plan *__restrict__ plan_
     const long long lo = leaf_start(P, b, i);
     const int len = (int)(leaf_start(P, b, i + 1) - lo);
     if (len == 0) return;
-    K *dst = (P.L[b] & 1) ? S : F;
+    K *dst = (P.L[b] & 1) ? S : F;  // where this bucket's merge level 0 reads
     const K kMax = KeyTraits<K>::kMax;
 
-    for (int j = tid; j < T; j += NT) s[pad_idx(j)] = j < len ? src[lo + j] : kMax;
-    __syncthreads();
+    // coalesced loads straight into registers (any placement works before the
+    // first network); pads are kMax and sort to the end
+    const K *in = src + lo;
     K v[VT];
 #pragma unroll
-    for (int k = 0; k < VT; ++k) v[k] = s[pad_idx(tid * VT + k)];
-    oddeven_sort<VT>(v);
-
-    // only as many passes as the tile needs: runs of width >= span are done
-    int span = VT;
-    while (span < len) span <<= 1;
-    for (int w = VT; w < span; w <<= 1) {
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < VT; ++k) s[pad_idx(tid * VT + k)] = v[k];
-        __syncthreads();
-        const int gd = tid * VT;
-        const int ps = gd & ~(2 * w - 1);
-        const int diag = gd - ps;
-        const int a0 = ps, b0 = ps + w;
-        int l = diag - w > 0 ? diag - w : 0;
-        int r = diag < w ? diag : w;
-        while (l < r) {
-            const int mid = (l + r) >> 1;
-            if (s[pad_idx(a0 + mid)] <= s[pad_idx(b0 + diag - 1 - mid)]) l = mid + 1;
-            else r = mid;
-        }
-        int ai = a0 + l, bi = b0 + diag - l;
-        const int ae = a0 + w, be = b0 + w;
-        K av = ai < ae ? s[pad_idx(ai)] : kMax;
-        K bv = bi < be ? s[pad_idx(bi)] : kMax;
-#pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            const bool takeA = (bi >= be) || (ai < ae && av <= bv);
-            v[k] = takeA ? av : bv;
-            if (takeA) {
-                ++ai;
-                if (ai < ae) av = s[pad_idx(ai)];
-            } else {
-                ++bi;
-                if (bi < be) bv = s[pad_idx(bi)];
-            }
-        }
+    for (int k = 0; k < VT; ++k) {
+        const int j = k * NT + tid;
+        v[k] = j < len ? in[j] : kMax;
     }
-    __syncthreads();
+    reg_sort<K, VT>(v);
+    bitonic_passes<K, NT, VT, 1>(sm, tid, v);
+
+    // thread t holds sorted elements t*VT .. t*VT+VT-1: transpose through
+    // padded shared memory for coalesced stores
 #pragma unroll
-    for (int k = 0; k < VT; ++k) s[pad_idx(tid * VT + k)] = v[k];
+    for (int k = 0; k < VT; ++k) sm[pad_idx(tid * VT + k)] = v[k];
     __syncthreads();
-    for (int j = tid; j < len; j += NT) dst[lo + j] = s[pad_idx(j)];
+    K *out = dst + lo;
+#pragma unroll 4
+    for (int j = tid; j < len; j += NT) out[j] = sm[pad_idx(j)];
+    (void)T;
 }
 
 // =============================================================== launchers
@@ -114,14 +228,16 @@ template <typename K>
 struct SGeo;
 template <>
 struct SGeo<int32_t> {
-    static constexpr int kNT = 512, kVT = 16;
+    static constexpr int kNT = HS_SORT_NT, kVT = HS_SORT_VT;  // default 256 x 32 = 8192 keys
 };
 template <>
 struct SGeo<int64_t> {
-    static constexpr int kNT = 512, kVT = 8;
+    static constexpr int kNT = HS_SORT_NT64, kVT = HS_SORT_VT64;  // default 256 x 16 = 4096 keys
 };
 
-int sort_tile_keys(int dt) { return dt == 0 ? SGeo<int32_t>::kNT * SGeo<int32_t>::kVT : SGeo<int64_t>::kNT * SGeo<int64_t>::kVT; }
+int sort_tile_keys(int dt) {
+    return dt == 0 ? SGeo<int32_t>::kNT * SGeo<int32_t>::kVT : SGeo<int64_t>::kNT * SGeo<int64_t>::kVT;
+}
 
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st) {
     k_plan<<<1, 32, 0, st>>>(user_off, ctl, log2c, mode, tile_keys);
@@ -132,8 +248,19 @@ template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
                                cudaStream_t st) {
     using G = SGeo<K>;
+    constexpr int T = G::kNT * G::kVT;
+    constexpr size_t smem = (size_t)(T + T / 32) * sizeof(K);  // padded transpose / cross-warp exchange
+    auto kern = k_tile_sort<K, G::kNT, G::kVT>;
+    static int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured_dev = dev;
+    }
     if (max_tiles <= 0) return cudaSuccess;
-    k_tile_sort<K, G::kNT, G::kVT><<<(unsigned)max_tiles, G::kNT, 0, st>>>(plan, (const K *)src, (K *)F, (K *)S);
+    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S);
     return cudaGetLastError();
 }
 

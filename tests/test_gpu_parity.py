@@ -341,3 +341,23 @@ def test_config_full_sampled(name):
         lo, hi = int(ref_off[b]), int(ref_off[b + 1])
         bucket = keys[(np.clip(keys // 10 ** (cfg.num_digits - 1), 0, 9)) == b]
         assert_same(got[lo:hi], O.quicksort(bucket), f"bucket {b}")
+
+
+@pytest.mark.parametrize("dtype,shift", [(np.int32, 1), (np.int32, 2), (np.int32, 3), (np.int64, 1)])
+def test_merge_and_chunks_misaligned_views(dtype, shift):
+    """Sub-tensor views whose start is not 16-byte aligned (bulk-copy phase != 0)."""
+    n = 6 * 4096 + 77
+    hi, D = (10**9, 9) if dtype == np.int32 else (10**18, 18)
+    keys = W.uniform(n, 1000 + shift, hi, dtype=dtype)
+    part, off = O.msd_partition(keys, D)
+    part = part.astype(dtype)
+    full = dev(np.concatenate([np.zeros(shift, dtype), part, np.zeros(5, dtype)]))
+    view = full[shift:shift + n]
+    d_off = dev(off)
+    hs.hs_sort_chunks(view, d_off, 4, out=view)
+    cs = O.sort_chunks(part, off, 4)
+    assert_same(host(view), cs, "chunks in place")
+    hs.hs_merge(view, d_off, 4, out=view)
+    got = host(full)
+    assert_same(got[shift:shift + n], O.merge(cs, off, 4), "merge in place")
+    assert np.all(got[:shift] == 0) and np.all(got[shift + n:] == 0)
