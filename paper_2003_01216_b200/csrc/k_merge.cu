@@ -22,13 +22,19 @@
 #include "hs_launch.h"
 
 #ifndef HS_MERGE_NT
-#define HS_MERGE_NT 256
+#define HS_MERGE_NT 128
 #endif
 #ifndef HS_MERGE_VT
-#define HS_MERGE_VT 16
+#define HS_MERGE_VT 25
+#endif
+#ifndef HS_MERGE_VT64
+#define HS_MERGE_VT64 13
+#endif
+#ifndef HS_PART_G
+#define HS_PART_G 1
 #endif
 #ifndef HS_MERGE_ST
-#define HS_MERGE_ST 3
+#define HS_MERGE_ST 2
 #endif
 
 namespace hs {
@@ -37,11 +43,12 @@ template <typename K>
 struct MGeo;
 template <>
 struct MGeo<int32_t> {
-    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT, kST = HS_MERGE_ST;  // default 256 x 16, 3 stages
+    // odd VT: lanes' merge positions (spaced ~VT/2 words) spread over all banks
+    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT, kST = HS_MERGE_ST;  // default 128 x 25, 2 stages
 };
 template <>
 struct MGeo<int64_t> {
-    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT / 2, kST = HS_MERGE_ST;
+    static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT64, kST = HS_MERGE_ST;
 };
 
 template <typename K>
@@ -61,13 +68,26 @@ __device__ __forceinline__ void load_plan_m(Plan &dst, const Plan *src) {
 }
 
 // =================================================================== K6a
-template <typename K>
+// Co-rank (merge-path) search for every TM-aligned output boundary of one
+// merge level: corank[beta] = absolute index into run A of the split of
+// output position beta*TM inside its pair (ties: A first, stable-left S:49).
+// G lanes cooperate on one boundary with a (G+1)-ary search: each round every
+// lane probes one candidate, a ballot finds the crossing, and the range
+// shrinks ~G+1 fold, so a 2^24-element pair takes ~6 rounds of parallel
+// probes instead of 24 dependent ones.
+template <typename K, int G>
 __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0, int *corank, int level,
                                   int n, int TM, int nbounds) {
+    static_assert(G >= 1 && G <= 32 && (32 % G) == 0, "group size");
     __shared__ Plan P;
     load_plan_m(P, plan_g);
     __syncthreads();
-    const int beta = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int beta = gtid / G;
+    const int j = gtid % G;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - j));
+    // whole groups take the same path (beta, x, bucket are group-uniform)
     if (beta >= nbounds) return;
     const long long x = (long long)beta * TM;
     if (x >= n) return;
@@ -77,16 +97,21 @@ __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, c
     const K *src = (level == 0 && src0) ? src0 : level_src(P, b, level, F, S);
     const long long diag = x - g.a_lo;
     const long long na = g.b_lo - g.a_lo, nb = g.b_hi - g.b_lo;
-    long long l = diag - nb > 0 ? diag - nb : 0;
+    long long l = diag - nb > 0 ? diag - nb : 0;  // answer in [l, r]; P(l) holds
     long long r = diag < na ? diag : na;
     const K *A = src + g.a_lo;
     const K *B = src + g.b_lo;
     while (l < r) {
-        const long long mid = (l + r) >> 1;
-        if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
-        else r = mid;
+        const long long step = (r - l + G) / (G + 1);  // >= 1
+        const long long c = l + (long long)(j + 1) * step;
+        const bool p = (c <= r) && (A[c - 1] <= B[diag - c]);
+        const unsigned m = __ballot_sync(gmask, p) >> (lane - j);
+        const int cnt = __popc(m);  // probes are monotone: the true ones form a prefix
+        const long long fail = l + (long long)(cnt + 1) * step;  // first false probe (or past r)
+        l += (long long)cnt * step;
+        if (cnt < G && fail - 1 < r) r = fail - 1;  // a probe failed: the answer is below it
     }
-    corank[beta] = (int)(g.a_lo + l);
+    if (j == 0) corank[beta] = (int)(g.a_lo + l);
 }
 
 // =================================================================== K6b
@@ -289,13 +314,16 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
         consumer_bar(NC);
         const int end = sh + q.len;
         if (diag < q.len) {
-            if (tid * VT >= sh && (tid + 1) * VT <= end) {
+            if (VT % E == 0 && tid * VT >= sh && (tid + 1) * VT <= end) {
 #pragma unroll
-                for (int k = 0; k < VT; k += E) {
+                for (int k = 0; k < (VT % E == 0 ? VT : 0); k += E) {
                     int4 w;
                     memcpy(&w, &v[k], 16);
                     *reinterpret_cast<int4 *>(sOut + tid * VT + k) = w;
                 }
+            } else if (tid * VT >= sh && (tid + 1) * VT <= end) {
+#pragma unroll
+                for (int k = 0; k < VT; ++k) sOut[tid * VT + k] = v[k];  // VT odd: conflict-free
             } else {
 #pragma unroll
                 for (int k = 0; k < VT; ++k) {
@@ -367,8 +395,10 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
     const int nbounds = nblocks + 1;
-    k_merge_partition<K><<<(nbounds + 255) / 256, 256, 0, st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank, level,
-                                                                n, TM, nbounds);
+    constexpr int PG = HS_PART_G;
+    const long long pthreads = (long long)nbounds * PG;
+    k_merge_partition<K, PG><<<(unsigned)((pthreads + 255) / 256), 256, 0, st>>>(plan, (K *)F, (K *)S, (const K *)src0,
+                                                                               corank, level, n, TM, nbounds);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long grid = (long long)per_sm * num_sms;
