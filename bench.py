@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py -- Gkeys/s of the hybrid MSD-radix / merge sort hot path on B200.
+
+One step = one hs_sort (C ABI, all kernels of the path: tile histograms,
+lookback prefix, stable scatter, tile sort, merge levels) over one batch of
+the BASELINE.json workload: C3 = 268,435,456 int32 keys uniform in [0, 1e9)
+(seed 3, D = 9, 8 chunks per bucket), keys resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+N > 1 runs N independent replicas (one per GPU, launched by torchrun; the
+path does not shard -- DESIGN.md §7), timed as the max over ranks.
+--impl reference times the CPU oracle (oracle/, the plain C implementation
+of the paper's algorithm) on bounded samples of the same workload.
+
+Prints ONE JSON line on rank 0 (details on stderr).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gkeys/s end-to-end sort on 1 B200; per-kernel HBM GB/s vs peak"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_desc(cfg):
+    kind = "uniform in [0, %d)" % cfg.value_range if cfg.kind == "uniform" else "70/20/10 normal/1024-value/uniform mixture"
+    return (f"{cfg.name}: {cfg.n:,} {cfg.dtype} keys, {kind}, seed {cfg.seed}, "
+            f"D={cfg.num_digits} (MSD digit = floor(k/10^{cfg.num_digits - 1})), {cfg.chunks} chunks/bucket")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, torch_dev_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(torch_dev_index)
+            bus = "%08x:%02x:%02x.0" % (getattr(props, "pci_domain_id", 0), props.pci_bus_id, props.pci_device_id)
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_dev_index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report null clocks
+            log(f"[bench] NVML unavailable: {e}")
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return None
+        reasons = sorted(self.reasons - {"gpu_idle"})
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- reference
+def run_reference(args, cfg):
+    import oracle
+    import workload as W
+    sample = min(cfg.n, args.ref_sample)
+    nsteps = args.warmup + args.steps
+    times = []
+    threads = 1
+    for i in range(nsteps):
+        start = (i * sample) % max(cfg.n - sample + 1, 1)
+        keys = W.generate(cfg, start, sample)
+        _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
+        if i >= args.warmup:
+            times.append(dt)
+    sec = statistics.mean(times)
+    value = sample / sec / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gkeys/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic",
+        "config": {"workload": workload_desc(cfg), "sample_keys_per_step": sample,
+                   "parallelism": "single host thread (plain oracle)"},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{sample:,} consecutive keys of {cfg.name} per step (bounded sample), "
+                                   "plain single-thread C oracle (gcc -O2), time of the sort call only"},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- ours
+def cpu_baseline(cfg, sample):
+    import oracle
+    import workload as W
+    keys = W.generate(cfg, 0, sample)
+    _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
+    return {"value": sample / dt / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {sample:,} keys of {cfg.name} ({sample / cfg.n:.3g} of the workload), plain "
+                      f"single-thread C oracle (gcc -O2), {dt:.2f} s for the sort call only"}
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import paper_2003_01216_b200 as hs
+    import workload as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    hs.load()
+    dt_code = 0 if cfg.dtype == "int32" else 1
+    tdt = torch.int32 if cfg.dtype == "int32" else torch.int64
+    ksize = 4 if cfg.dtype == "int32" else 8
+
+    # inputs: generated on the host (seeded), pinned, copied once to HBM
+    h_in = torch.empty(cfg.n, dtype=tdt, pin_memory=True)
+    W.generate(cfg, 0, cfg.n, out=h_in.numpy())
+    h_out = torch.empty_like(h_in, pin_memory=True)
+    src = h_in.to(dev)
+    buf = torch.empty_like(src)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def sort_step():
+        hs.hs_sort(buf, cfg.num_digits, cfg.chunks)
+
+    def restore():
+        buf.copy_(src)
+        flush.fill_(1)
+
+    for _ in range(args.warmup):
+        restore()
+        sort_step()
+    torch.cuda.synchronize()
+    ok = bool(torch.all(buf[1:] >= buf[:-1]).item())
+    if not ok:
+        raise SystemExit("[bench] hs_sort output is not sorted")
+    launches_per_step = hs.last_launch_count()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- timed region: K steps, CUDA events around each hs_sort
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with sampler:
+        for i in range(args.steps):
+            restore()  # untimed: outside the event pair
+            evs[i][0].record(stream)
+            sort_step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = statistics.mean(step_ms)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * cfg.n / (ms * 1e-3) / 1e9
+
+    # ---- per-kernel device times (library events on the launching stream)
+    hs.profile_enable(True)
+    for _ in range(args.steps):
+        restore()
+        sort_step()
+    prof = hs.profile_read()
+    hs.profile_enable(False)
+    # algorithmic bytes of the dominant kernel from the plan of this workload
+    _, off = hs.hs_msd_partition(src, cfg.num_digits)
+    off_h = off.cpu().numpy()
+    levels, tile_levels = hs.plan_levels(off_h, dt_code, cfg.chunks, 0)
+    m = np.diff(off_h)
+    per_kernel = {}
+    for kind, (tot, cnt) in prof.items():
+        if cnt:
+            per_kernel[kind] = {"ms_per_step": tot / args.steps, "launches_per_step": cnt // args.steps}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"])
+    L_launch = per_kernel.get("merge_level", {}).get("launches_per_step", 0)
+    level_bytes = [2 * ksize * int(sum(m[b] for b in range(10) if levels[b] > lv)) for lv in range(L_launch)]
+    alg = {  # algorithmic bytes per step of each kernel kind
+        "tile_hist": ksize * cfg.n, "scatter": 2 * ksize * cfg.n, "tile_sort": 2 * ksize * cfg.n,
+        "merge_level": sum(level_bytes),
+    }
+    for k, d in per_kernel.items():
+        if k in alg and d["ms_per_step"] > 0:
+            d["alg_GBps"] = alg[k] / (d["ms_per_step"] * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    achieved = per_kernel[dom].get("alg_GBps")
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(dom)
+    active = [b for b in level_bytes if b > 0]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": (statistics.mean(active) if dom == "merge_level" and active else alg.get(dom)),
+                "launches_per_step": per_kernel[dom]["launches_per_step"],
+                "active_launches_per_step": len(active) if dom == "merge_level" else 1}
+    path_bytes = ksize * cfg.n * 5 + sum(level_bytes)  # hist r + scatter r/w + tile sort r/w + levels
+    step_roof = {"alg_bytes_per_step": path_bytes, "t_roof_ms": path_bytes / (peak * 1e9) * 1e3,
+                 "frac": path_bytes / (peak * 1e9) / (ms * 1e-3), "levels": max(levels)}
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        buf.copy_(h_in, non_blocking=True)
+        sort_step()
+        h_out.copy_(buf, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e = statistics.mean(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    ok_e2e = bool(np.all(h_out.numpy()[1:] >= h_out.numpy()[:-1]))
+
+    if rank == 0:
+        log(f"[bench] {cfg.name} hs_sort {ms:.3f} ms/step = {value:.2f} Gkeys/s (steps {[round(x, 3) for x in step_ms]}), "
+            f"wall {wall:.3f} s; e2e {e2e:.3f} ms (sorted={ok_e2e})")
+        for k, d in sorted(per_kernel.items(), key=lambda kv: -kv[1]["ms_per_step"]):
+            log(f"[bench]   {k:16s} {d['ms_per_step']:8.3f} ms/step  {d['launches_per_step']:3d} launches  "
+                f"{d.get('alg_GBps', 0):7.0f} GB/s alg")
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, min(cfg.n, args.cpu_sample))
+            log(f"[bench] cpu_baseline {cpu}")
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "n_per_gpu": cfg.n, "num_digits": cfg.num_digits,
+                       "chunks_per_bucket": cfg.chunks, "merge_levels": max(levels),
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "flushed (256 MiB device write) before every timed step; input 1 GiB > L2",
+                       "timing": "mean of per-step CUDA-event intervals around hs_sort on the launching stream; "
+                                 "the untimed input restore + L2 flush sit between the intervals; max over ranks"},
+            "roofline": roofline,
+            "path_roofline": step_roof,
+            "kernels": per_kernel,
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * cfg.n / (e2e * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": e2e,
+                    "h2d_bytes_per_step": cfg.n * ksize, "d2h_bytes_per_step": cfg.n * ksize,
+                    "how": "pinned host keys -> H2D -> hs_sort -> D2H, CUDA events on the stream, max over ranks"},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": sampler.result(),
+            "sorted_check": ok and ok_e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--ref-sample", type=int, default=1 << 23)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    import workload as W
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

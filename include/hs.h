@@ -160,6 +160,28 @@ int hs_abi_version(void);
 int hs_last_launch_count(void);
 int hs_tile_keys(hs_dtype_t dtype, int which /* 0 scatter, 1 tile sort, 2 merge */);
 
+/*
+ * Per-kernel timing (bench only): while enabled on the calling host thread,
+ * every kernel the library launches is bracketed by two CUDA events recorded
+ * on the launching stream.  hs_profile_read synchronises on them, writes
+ * per-kind total milliseconds and launch counts for kinds [0, nkinds) and
+ * forgets them; returns 0, or -1 if an event query failed.  Kind names:
+ * hs_profile_kind_name(k), k = 0 .. 7 (tile_hist, tile_scan, scatter, plan,
+ * tile_sort, merge_partition, merge_level, copy).
+ */
+int hs_profile_enable(int on);
+int hs_profile_read(double *ms, int *count, int nkinds);
+const char *hs_profile_kind_name(int kind);
+
+/*
+ * Host-side replica of the device plan (bench / tests): from HOST
+ * bucket_offsets[11], the merge levels L[b] each bucket runs and its leaf
+ * exponent k[b] (chunk = 2^k[b] tile-sort leaves) for mode 0 = hs_sort,
+ * 1 = hs_sort_chunks, 2 = hs_merge.  Returns max L, or -1 on a bad argument.
+ */
+int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chunks_per_bucket, int mode,
+                   int *levels_out, int *tile_levels_out);
+
 #ifdef __cplusplus
 }
 #endif

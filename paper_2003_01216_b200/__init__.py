@@ -29,7 +29,9 @@ STATUS = {0: "HS_OK", 1: "HS_ERR_INVALID_VALUE", 2: "HS_ERR_UNSUPPORTED_DTYPE", 
 EXPORTED_SYMBOLS = (
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_status_string",
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
+    "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels",
 )
+PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy")
 
 
 class HybridSortError(RuntimeError):
@@ -70,6 +72,14 @@ def load(path: str | None = None):
     lib.hs_last_launch_count.restype = ci
     lib.hs_tile_keys.argtypes = [ci, ci]
     lib.hs_tile_keys.restype = ci
+    lib.hs_profile_enable.argtypes = [ci]
+    lib.hs_profile_enable.restype = ci
+    lib.hs_profile_read.argtypes = [vp, vp, ci]
+    lib.hs_profile_read.restype = ci
+    lib.hs_profile_kind_name.argtypes = [ci]
+    lib.hs_profile_kind_name.restype = ctypes.c_char_p
+    lib.hs_plan_levels.argtypes = [vp, ci, ci, ci, vp, vp]
+    lib.hs_plan_levels.restype = ci
     if path is None:
         _LIB = lib
     return lib
@@ -92,6 +102,33 @@ def last_launch_count() -> int:
 
 def tile_keys(dtype_code: int, which: int) -> int:
     return int(load().hs_tile_keys(dtype_code, which))
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library kernel with CUDA events on its stream (this thread)."""
+    load().hs_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kind: (total_ms, launches)} since the last read (synchronises)."""
+    import numpy as np
+    n = len(PROFILE_KINDS)
+    ms = np.zeros(n, dtype=np.float64)
+    cnt = np.zeros(n, dtype=np.int32)
+    if load().hs_profile_read(ms.ctypes.data, cnt.ctypes.data, n) != 0:
+        raise HybridSortError(4, "event timing failed")
+    return {PROFILE_KINDS[i]: (float(ms[i]), int(cnt[i])) for i in range(n)}
+
+
+def plan_levels(bucket_offsets_host, dtype_code: int, chunks: int, mode: int = 0):
+    """(levels[10], tile_levels[10]) of the device plan, computed on the host."""
+    import numpy as np
+    off = np.ascontiguousarray(np.asarray(bucket_offsets_host, dtype=np.int64))
+    L = np.zeros(10, dtype=np.int32)
+    k = np.zeros(10, dtype=np.int32)
+    if load().hs_plan_levels(off.ctypes.data, dtype_code, chunks, mode, L.ctypes.data, k.ctypes.data) < 0:
+        raise ValueError("bad plan arguments")
+    return L.tolist(), k.tolist()
 
 
 # ------------------------------------------------------------ tensor glue

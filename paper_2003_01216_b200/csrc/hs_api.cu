@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "hs.h"
 #include "hs_device.cuh"
@@ -185,9 +186,100 @@ int level_bound(long long n, int log2c, int T, int with_tiles, int with_tree) {
 
 long long tile_bound(long long n, long long c, int T) { return 2 * ((n + T - 1) / T) + 50 * c; }
 
+// ------------------------------------------------------------- profiling
+struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+};
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+thread_local cudaEvent_t g_prof_open = nullptr;
+
+cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+const char *const kProfNames[hs::kProfKinds] = {"tile_hist", "tile_scan", "scatter", "plan",
+                                                 "tile_sort", "merge_partition", "merge_level", "copy"};
+
 }  // namespace
 
+namespace hs {
+void prof_begin(int kind, cudaStream_t st) {
+    (void)kind;
+    if (!g_prof_on) return;
+    g_prof_open = prof_event();
+    cudaEventRecord(g_prof_open, st);
+}
+void prof_end(int kind, cudaStream_t st) {
+    if (!g_prof_on || !g_prof_open) return;
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, st);
+    g_prof_recs.push_back({kind, g_prof_open, b});
+    g_prof_open = nullptr;
+}
+}  // namespace hs
+
 extern "C" {
+
+int hs_profile_enable(int on) {
+    g_prof_on = on != 0;
+    return 0;
+}
+
+int hs_profile_read(double *ms, int *count, int nkinds) {
+    for (int k = 0; k < nkinds; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (count) count[k] = 0;
+    }
+    int rc = 0;
+    for (const ProfRec &r : g_prof_recs) {
+        float t = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) rc = -1;
+        if (r.kind >= 0 && r.kind < nkinds) {
+            if (ms) ms[r.kind] += t;
+            if (count) count[r.kind] += 1;
+        }
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    g_prof_recs.clear();
+    return rc;
+}
+
+const char *hs_profile_kind_name(int kind) { return (kind >= 0 && kind < hs::kProfKinds) ? kProfNames[kind] : ""; }
+
+int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chunks_per_bucket, int mode,
+                   int *levels_out, int *tile_levels_out) {
+    if (dtype != HS_INT32 && dtype != HS_INT64) return -1;
+    int log2c;
+    if (check_chunks(chunks_per_bucket, &log2c) != HS_OK) return -1;
+    const long long c = 1LL << log2c;
+    const long long T = hs::sort_tile_keys((int)dtype);
+    int lmax = 0;
+    for (int b = 0; b < 10; ++b) {
+        const long long m = bucket_offsets_host[b + 1] - bucket_offsets_host[b];
+        int k = 0;
+        if (mode != hs::kPlanMerge) {
+            const long long cm = (m + c - 1) / c;
+            const long long tiles = (cm + T - 1) / T;
+            k = tiles > 1 ? ceil_log2(tiles) : 0;
+        }
+        const int L = mode == hs::kPlanSort ? k + log2c : (mode == hs::kPlanChunks ? k : log2c);
+        if (levels_out) levels_out[b] = L;
+        if (tile_levels_out) tile_levels_out[b] = k;
+        lmax = L > lmax ? L : lmax;
+    }
+    return lmax;
+}
 
 const char *hs_status_string(hs_status_t s) {
     switch (s) {

@@ -11,6 +11,13 @@ namespace hs {
 struct Ctl;
 struct Plan;
 
+// Optional per-kernel CUDA-event timing (hs_profile_enable); kinds match
+// hs_profile_kind_name().  No-ops unless enabled on the calling thread.
+enum ProfKind { kProfTileHist = 0, kProfTileScan, kProfScatter, kProfPlan, kProfTileSort, kProfMergePartition,
+                kProfMergeLevel, kProfCopy, kProfKinds };
+void prof_begin(int kind, cudaStream_t st);
+void prof_end(int kind, cudaStream_t st);
+
 int scatter_tile_keys(int dt);  // keys per K1/K3 tile
 int sort_tile_keys(int dt);     // leaf-tile capacity T of K5
 int merge_span(int dt);         // outputs per K6 piece (TM)

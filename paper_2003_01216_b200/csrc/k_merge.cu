@@ -397,14 +397,18 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     const int nbounds = nblocks + 1;
     constexpr int PG = HS_PART_G;
     const long long pthreads = (long long)nbounds * PG;
+    prof_begin(kProfMergePartition, st);
     k_merge_partition<K, PG><<<(unsigned)((pthreads + 255) / 256), 256, 0, st>>>(plan, (K *)F, (K *)S, (const K *)src0,
                                                                                corank, level, n, TM, nbounds);
+    prof_end(kProfMergePartition, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long grid = (long long)per_sm * num_sms;
     if (grid > nblocks) grid = nblocks;
+    prof_begin(kProfMergeLevel, st);
     kern<<<(unsigned)grid, G::kNT + 32, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank, level, n,
                                                            nblocks);
+    prof_end(kProfMergeLevel, st);
     return cudaGetLastError();
 }
 
@@ -413,7 +417,9 @@ cudaError_t launch_copy_t(const void *src, void *dst, long long n, int num_sms, 
     if (n <= 0) return cudaSuccess;
     long long want = (n + 255) / 256;
     int grid = (int)(want > 8LL * num_sms ? 8LL * num_sms : want);
+    prof_begin(kProfCopy, st);
     k_copy<K><<<grid, 256, 0, st>>>((const K *)src, (K *)dst, n);
+    prof_end(kProfCopy, st);
     return cudaGetLastError();
 }
 

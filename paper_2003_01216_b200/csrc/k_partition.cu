@@ -460,14 +460,18 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     if (ntiles > 0) {
         long long want = (ntiles + kHistWarps - 1) / kHistWarps;
         int grid = (int)(want > 8LL * num_sms ? 8LL * num_sms : want);
+        prof_begin(kProfTileHist, st);
         k_tile_hist<K, TP><<<grid, kHistWarps * 32, 0, st>>>((const K *)keys, n, h, dp, tile_hist, (int)ntiles);
+        prof_end(kProfTileHist, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     const long long per = (long long)kScanNT * kScanIPT;
     const int sgrid = (int)(ntiles > 0 ? (ntiles + per - 1) / per : 1);
+    prof_begin(kProfTileScan, st);
     k_tile_scan<<<sgrid, kScanNT, 0, st>>>(tile_hist, tile_pref, (int)ntiles, status, ctl, user_off, plan_mode, log2c,
                                            sort_tile_keys);
+    prof_end(kProfTileScan, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
@@ -487,8 +491,10 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     }
     long long grid = (long long)per_sm * num_sms;
     if (grid > ntiles) grid = ntiles;
+    prof_begin(kProfScatter, st);
     kern<<<(unsigned)grid, G::kScatNT, SS::bytes(), st>>>((const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
                                                           (int)ntiles);
+    prof_end(kProfScatter, st);
     return cudaGetLastError();
 }
 

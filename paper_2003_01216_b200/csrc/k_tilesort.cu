@@ -240,7 +240,9 @@ int sort_tile_keys(int dt) {
 }
 
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st) {
+    prof_begin(kProfPlan, st);
     k_plan<<<1, 32, 0, st>>>(user_off, ctl, log2c, mode, tile_keys);
+    prof_end(kProfPlan, st);
     return cudaGetLastError();
 }
 
@@ -260,7 +262,9 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
         configured_dev = dev;
     }
     if (max_tiles <= 0) return cudaSuccess;
+    prof_begin(kProfTileSort, st);
     kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S);
+    prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }
 
