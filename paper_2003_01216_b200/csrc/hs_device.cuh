@@ -265,23 +265,32 @@ __device__ __forceinline__ void cas(K &a, K &b) {
     b = hi;
 }
 
-// Batcher odd-even merge sort network on N registers (all indices are
-// compile-time after unrolling, so v stays in registers).
+// Batcher odd-even merge sort network on N registers.  The comparator list
+// is generated at compile time (comparators touching an index >= N are
+// dropped, i.e. the input is padded with +inf, valid for any N), so the
+// unrolled loop below has constant register indices and v stays in registers.
+template <int N>
+struct OddEvenNet {
+    int a[N * N], b[N * N];
+    int n;
+    constexpr OddEvenNet() : a(), b(), n(0) {
+        for (int p = 1; p < N; p <<= 1)
+            for (int k = p; k >= 1; k >>= 1)
+                for (int j = k % p; j + k < N; j += 2 * k)
+                    for (int i = 0; i < k; ++i)
+                        if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+                            a[n] = i + j;
+                            b[n] = i + j + k;
+                            ++n;
+                        }
+    }
+};
+
 template <int N, typename K>
 __device__ __forceinline__ void oddeven_sort(K (&v)[N]) {
+    constexpr OddEvenNet<N> net{};
 #pragma unroll
-    for (int p = 1; p < N; p <<= 1) {
-#pragma unroll
-        for (int k = p; k >= 1; k >>= 1) {
-#pragma unroll
-            for (int j = k % p; j + k < N; j += 2 * k) {
-#pragma unroll
-                for (int i = 0; i < k; ++i) {
-                    if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p)) cas(v[i + j], v[i + j + k]);
-                }
-            }
-        }
-    }
+    for (int c = 0; c < net.n; ++c) cas(v[net.a[c]], v[net.b[c]]);
 }
 
 }  // namespace hs

@@ -13,28 +13,32 @@
 // sorted lists pairwise" idea its parallel sorts are built from:
 //   1. each thread sorts VT keys in registers (Batcher odd-even network,
 //      compile-time register indices, no branches);
-//   2. log2(T/VT) bitonic merge passes: strides inside a warp use warp
-//      shuffles, strides across warps exchange through shared memory.
+//   2. log2(NT) merge-path merge rounds in shared memory turn the NT sorted
+//      runs into one (the binary-tree merge of P:58-60 at CTA scope).
 // Keys-only data makes the sorted tile unique, so the (unstable) network
-// order is unobservable.  The tile is padded to a power of two with the
-// dtype maximum; pads sort to the end and are never stored (they equal any
-// real maximum key, so the stored prefix is the same multiset).
+// order is unobservable.
 #include <cstdint>
 
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
 #ifndef HS_SORT_NT
-#define HS_SORT_NT 256
+#define HS_SORT_NT 512
 #endif
 #ifndef HS_SORT_VT
-#define HS_SORT_VT 32
+#define HS_SORT_VT 27
+#endif
+#ifndef HS_SORT_MINB
+#define HS_SORT_MINB 2
 #endif
 #ifndef HS_SORT_NT64
-#define HS_SORT_NT64 256
+#define HS_SORT_NT64 512
 #endif
 #ifndef HS_SORT_VT64
-#define HS_SORT_VT64 16
+#define HS_SORT_VT64 15
+#endif
+#ifndef HS_SORT_MINB64
+#define HS_SORT_MINB64 2
 #endif
 
 namespace hs {
@@ -57,137 +61,71 @@ __global__ void k_plan(const long long *__restrict__ user_off, Ctl *ctl, int log
 }
 
 // =================================================================== K5
-// Bitonic tile sort.  Logical element e = t*VT + k lives in register k of
-// thread t.  Sorting runs of width W into runs of 2W ("pass W") is one
-// bitonic merge: a mirror stage (e <-> the mirror of e inside its 2W block,
-// lower half keeps the min) followed by half-cleaner stages of stride
-// W/2 .. 1 (lower index keeps the min).  A stride of S elements is
-//   S <  VT        : inside a thread  -> compare-exchange of two registers
-//   S >= VT, lanes : inside a warp    -> __shfl_xor_sync + predicated min/max
-//   S >= 32*VT     : across warps     -> exchange through shared memory
-// No stage depends on the data, so there are no searches and no
-// data-dependent shared-memory addresses.
+// Block merge sort of one leaf tile in shared memory.
+//   1. one 1-D bulk async copy (TMA engine) brings the leaf (a 16-byte aligned
+//      superset of it) into shared memory; positions past the leaf are filled
+//      with the dtype maximum (pads sort to the end, are never stored, and
+//      equal any real maximum key, so the stored prefix is the same multiset);
+//   2. thread t takes the VT consecutive keys t*VT .. t*VT+VT-1 (VT odd, so
+//      the blocked reads and writes of a warp hit 32 distinct banks) and sorts
+//      them in registers with Batcher's odd-even network (compile-time
+//      register indices, no branches);
+//   3. log2(NT) merge rounds: runs of R*VT keys are merged pairwise; every
+//      thread finds the start of its VT outputs by a merge-path binary search
+//      over the two runs in shared memory (ties take A) and merges VT
+//      keys serially into registers.  Real keys always occupy positions
+//      [0, len) (induction over the rounds), so a thread whose VT outputs all
+//      lie at or past len skips the round (ragged leaves cost what they hold);
+//   4. the sorted tile goes back to shared memory at the destination's 16-byte
+//      phase and leaves with one 1-D bulk async store (+ scalar head/tail).
+// This is the GPU shape of the paper's "sort partitions, then merge sorted
+// lists pairwise in a binary tree" at CTA scope.
 template <typename K>
 __device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
 template <typename K>
 __device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
 
+__device__ __forceinline__ void bulk_s2g_ts(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// Merge-path split of output diag between A = sm[a0, a0+na) and B = sm[b0, b0+nb) (stable-left).
 template <typename K>
-__device__ __forceinline__ K shfl_xor_k(K v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
-
-// Half-cleaner stages with stride < VT (registers only).
-template <typename K, int VT>
-__device__ __forceinline__ void intra_stages(K (&v)[VT]) {
-#pragma unroll
-    for (int sd = VT / 2; sd >= 1; sd >>= 1) {
-#pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            if ((k & sd) == 0) {
-                const K a = v[k], b = v[k + sd];
-                v[k] = kmin(a, b);
-                v[k + sd] = kmax(a, b);
-            }
-        }
+__device__ __forceinline__ int smem_merge_path(const K *sm, int a0, int na, int b0, int nb, int diag) {
+    int l = diag - nb > 0 ? diag - nb : 0;
+    int r = diag < na ? diag : na;
+    while (l < r) {
+        const int mid = (l + r) >> 1;
+        if (sm[a0 + mid] <= sm[b0 + diag - 1 - mid]) l = mid + 1;
+        else r = mid;
     }
-}
-
-// Cross-warp exchange through shared memory (register-major layout
-// sm[k*NT + t]: conflict-free).  partner thread pt, partner register
-// index pk(k) = MIRROR ? VT-1-k : k.
-template <typename K, int NT, int VT, bool MIRROR>
-__device__ __forceinline__ void smem_stage(K *sm, int tid, int pt, bool keep_min, K (&v)[VT]) {
-#pragma unroll
-    for (int k = 0; k < VT; ++k) sm[k * NT + tid] = v[k];
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const K o = sm[(MIRROR ? VT - 1 - k : k) * NT + pt];
-        v[k] = keep_min ? kmin(v[k], o) : kmax(v[k], o);
-    }
-    __syncthreads();
-}
-
-// Sort a thread's VT registers ascending: bitonic network with constant
-// register indices (mirror stage + half-cleaners per block size).
-template <typename K, int VT>
-__device__ __forceinline__ void reg_sort(K (&v)[VT]) {
-#pragma unroll
-    for (int size = 2; size <= VT; size <<= 1) {
-#pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            const int base = k & ~(size - 1), off = k - base;
-            if (off < size / 2) {
-                const int m = base + size - 1 - off;
-                const K a = v[k], b = v[m];
-                v[k] = kmin(a, b);
-                v[m] = kmax(a, b);
-            }
-        }
-#pragma unroll
-        for (int sd = size / 4; sd >= 1; sd >>= 1) {
-#pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                if ((k & sd) == 0 && ((k & (size - 1)) + sd) < size) {
-                    const K a = v[k], b = v[k + sd];
-                    v[k] = kmin(a, b);
-                    v[k + sd] = kmax(a, b);
-                }
-            }
-        }
-    }
-}
-
-// One bitonic merge pass turning runs of width W = VT*R into runs of 2W.
-template <typename K, int NT, int VT, int R>
-__device__ __forceinline__ void bitonic_pass(K *sm, int tid, K (&v)[VT]) {
-    const int lane = tid & 31;
-    // mirror stage: thread u (within its 2R-thread block) <-> 2R-1-u, register k <-> VT-1-k
-    const bool lower = (tid & R) == 0;
-    if constexpr (2 * R <= 32) {
-#pragma unroll
-        for (int k = 0; k < VT / 2; ++k) {
-            const K o1 = __shfl_xor_sync(0xffffffffu, v[VT - 1 - k], 2 * R - 1);
-            const K o2 = __shfl_xor_sync(0xffffffffu, v[k], 2 * R - 1);
-            v[k] = lower ? kmin(v[k], o1) : kmax(v[k], o1);
-            v[VT - 1 - k] = lower ? kmin(v[VT - 1 - k], o2) : kmax(v[VT - 1 - k], o2);
-        }
-    } else {
-        smem_stage<K, NT, VT, true>(sm, tid, tid ^ (2 * R - 1), lower, v);
-    }
-    // half-cleaners across threads: thread distance R/2 .. 1
-#pragma unroll
-    for (int d = R / 2; d >= 1; d >>= 1) {
-        const bool lo = (tid & d) == 0;
-        if (d >= 32) {
-            smem_stage<K, NT, VT, false>(sm, tid, tid ^ d, lo, v);
-        } else {
-#pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                const K o = __shfl_xor_sync(0xffffffffu, v[k], d);
-                v[k] = lo ? kmin(v[k], o) : kmax(v[k], o);
-            }
-        }
-    }
-    (void)lane;
-    intra_stages<K, VT>(v);
-}
-
-template <typename K, int NT, int VT, int R>
-__device__ __forceinline__ void bitonic_passes(K *sm, int tid, K (&v)[VT]) {
-    if constexpr (R < NT) {
-        bitonic_pass<K, NT, VT, R>(sm, tid, v);
-        bitonic_passes<K, NT, VT, 2 * R>(sm, tid, v);
-    }
+    return l;
 }
 
 template <typename K, int NT, int VT>
-__global__ void __launch_bounds__(NT) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S) {
-    constexpr int T = NT * VT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    K *const sm = reinterpret_cast<K *>(smem_raw);
+struct TSGeo {
+    static constexpr int T = NT * VT;
+    static constexpr int E = 16 / sizeof(K);
+    static constexpr size_t bytes() { return (size_t)(T + 2 * E) * sizeof(K); }
+};
+
+template <typename K, int NT, int VT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S) {
+    static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
+    using G = TSGeo<K, NT, VT>;
+    constexpr int T = G::T, E = G::E;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    K *const sbuf = reinterpret_cast<K *>(smem_raw);
     __shared__ Plan P;
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
     load_plan(P, plan_g);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
     __syncthreads();
     const long long g = blockIdx.x;
     if (g >= P.tile_prefix[10]) return;
@@ -197,30 +135,90 @@ __global__ void __launch_bounds__(NT) k_tile_sort(const Plan *__restrict__ plan_
     const long long lo = leaf_start(P, b, i);
     const int len = (int)(leaf_start(P, b, i + 1) - lo);
     if (len == 0) return;
-    K *dst = (P.L[b] & 1) ? S : F;  // where this bucket's merge level 0 reads
+    K *const out = ((P.L[b] & 1) ? S : F) + lo;  // where this bucket's merge level 0 reads
     const K kMax = KeyTraits<K>::kMax;
 
-    // coalesced loads straight into registers (any placement works before the
-    // first network); pads are kMax and sort to the end
+    // 1. bulk load of the 16-byte aligned superset of the leaf
     const K *in = src + lo;
-    K v[VT];
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int j = k * NT + tid;
-        v[k] = j < len ? in[j] : kMax;
+    const uintptr_t ga0 = (uintptr_t)in & ~(uintptr_t)15;
+    const uintptr_t ga1 = ((uintptr_t)(in + len) + 15) & ~(uintptr_t)15;
+    const int h = (int)(((uintptr_t)in - ga0) / sizeof(K));
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar, (uint32_t)(ga1 - ga0));
+        bulk_g2s(sbuf, (const void *)ga0, (uint32_t)(ga1 - ga0), &bar);
     }
-    reg_sort<K, VT>(v);
-    bitonic_passes<K, NT, VT, 1>(sm, tid, v);
-
-    // thread t holds sorted elements t*VT .. t*VT+VT-1: transpose through
-    // padded shared memory for coalesced stores
-#pragma unroll
-    for (int k = 0; k < VT; ++k) sm[pad_idx(tid * VT + k)] = v[k];
+    K *const sm = sbuf + h;  // sm[0 .. len) = the leaf
+    mbar_wait(&bar, 0);
+    for (int j = len + tid; j < T; j += NT) sm[j] = kMax;
     __syncthreads();
-    K *out = dst + lo;
-#pragma unroll 4
-    for (int j = tid; j < len; j += NT) out[j] = sm[pad_idx(j)];
-    (void)T;
+
+    // 2. register sort of VT consecutive keys
+    K v[VT];
+    const bool live0 = tid * VT < len;
+#pragma unroll
+    for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
+    if (live0) oddeven_sort<VT>(v);
+
+    // 3. merge rounds (R = threads per run)
+#pragma unroll 1
+    for (int R = 1; R < NT; R <<= 1) {
+        const bool live = tid * VT < len;
+        __syncthreads();  // everyone has read the previous round's runs
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
+        }
+        __syncthreads();
+        if (live) {
+            const int j = tid & (2 * R - 1);
+            const int a0 = (tid - j) * VT, run = R * VT, b0 = a0 + run;
+            const int diag = j * VT;
+            const int s = smem_merge_path(sm, a0, run, b0, run, diag);
+            const int a_end = b0, b_end = b0 + run;
+            int ai = a0 + s, bi = b0 + diag - s;
+            K x = ai < a_end ? sm[ai] : kMax;
+            K y = bi < b_end ? sm[bi] : kMax;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                const bool p = x <= y;
+                v[k] = p ? x : y;
+                if (k + 1 < VT) {
+                    const int nx = (p ? ai : bi) + 1;
+                    const int lim = p ? a_end : b_end;
+                    const K t = sm[nx];  // nx <= T: inside the buffer (T + 2E slots)
+                    const K tv = nx < lim ? t : kMax;
+                    ai = p ? nx : ai;
+                    bi = p ? bi : nx;
+                    x = p ? tv : x;
+                    y = p ? y : tv;
+                }
+            }
+        }
+    }
+
+    // 4. stage at the destination's 16-byte phase, bulk store the aligned middle
+    const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
+    K *const so = sbuf + sh;  // so[p] <-> out[p]
+    __syncthreads();
+    if (tid * VT < len) {
+#pragma unroll
+        for (int k = 0; k < VT; ++k) so[tid * VT + k] = v[k];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    const int m0 = sh == 0 ? 0 : E - sh;            // first output at a 16-byte aligned address
+    const int m1 = (sh + len) / E * E - sh;         // end of the aligned middle
+    if (m1 > m0) {
+        if (tid == 0) {
+            bulk_s2g_ts(out + m0, so + m0, (uint32_t)((m1 - m0) * sizeof(K)));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (tid < m0) out[tid] = so[tid];
+        else if (tid >= E && tid < 2 * E && m1 + tid - E < len) out[m1 + tid - E] = so[m1 + tid - E];
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else {
+        for (int p = tid; p < len; p += NT) out[p] = so[p];
+    }
 }
 
 // =============================================================== launchers
@@ -228,11 +226,11 @@ template <typename K>
 struct SGeo;
 template <>
 struct SGeo<int32_t> {
-    static constexpr int kNT = HS_SORT_NT, kVT = HS_SORT_VT;  // default 256 x 32 = 8192 keys
+    static constexpr int kNT = HS_SORT_NT, kVT = HS_SORT_VT, kMinB = HS_SORT_MINB;
 };
 template <>
 struct SGeo<int64_t> {
-    static constexpr int kNT = HS_SORT_NT64, kVT = HS_SORT_VT64;  // default 256 x 16 = 4096 keys
+    static constexpr int kNT = HS_SORT_NT64, kVT = HS_SORT_VT64, kMinB = HS_SORT_MINB64;
 };
 
 int sort_tile_keys(int dt) {
@@ -250,9 +248,8 @@ template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
                                cudaStream_t st) {
     using G = SGeo<K>;
-    constexpr int T = G::kNT * G::kVT;
-    constexpr size_t smem = (size_t)(T + T / 32) * sizeof(K);  // padded transpose / cross-warp exchange
-    auto kern = k_tile_sort<K, G::kNT, G::kVT>;
+    constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
+    auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
