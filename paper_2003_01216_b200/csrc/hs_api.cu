@@ -122,18 +122,20 @@ struct Workspace {
     uint32_t *tile_hist = nullptr;
     uint32_t *tile_pref = nullptr;
     int *corank = nullptr;
+    void *samp[2] = {nullptr, nullptr};  // key samples (ping-pong by merge level)
     size_t zero_bytes = 0;
 };
 
 hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
-                     cudaStream_t st) {
+                     size_t samp_bytes, cudaStream_t st) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
     size_t th = round_up(ntiles * 5 * 4, 256);
     size_t tp = round_up(ntiles * 10 * 4, 256);
     size_t k = round_up(corank_words * 4, 256);
-    size_t total = a + c + z + th + tp + k;
+    size_t sp = round_up(samp_bytes, 256);
+    size_t total = a + c + z + th + tp + k + 2 * sp;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -148,9 +150,16 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     w->tile_hist = (uint32_t *)(b + a + c + z);
     w->tile_pref = (uint32_t *)(b + a + c + z + th);
     w->corank = (int *)(b + a + c + z + th + tp);
+    if (samp_bytes) {
+        w->samp[0] = b + a + c + z + th + tp + k;
+        w->samp[1] = b + a + c + z + th + tp + k + sp;
+    }
     w->zero_bytes = c + z;
     return HS_OK;
 }
+
+// One generation of key samples (hs_device.cuh, kSampleQ).
+size_t samp_bytes(int64_t n, hs_dtype_t dt) { return (size_t)(n / hs::kSampleQ + 2) * ksize(dt); }
 
 #define HS_TRY_CUDA(expr, what)                                   \
     do {                                                          \
@@ -325,7 +334,7 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
     digit_params(num_digits, dtype, &div, &magic);
 
     Workspace ws;
-    if ((s = ws_alloc(&ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, 0, stream)) != HS_OK) return s;
     int launches = 0;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
     HS_TRY_CUDA(hs::launch_partition(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status,
@@ -362,7 +371,7 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
 
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
-                      (size_t)nblocks + 2, stream)) != HS_OK)
+                      (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
         return s;
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
@@ -373,12 +382,13 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
                 "K1-K3 partition");
     launches += 2;
     // a5: leaf-tile sort S -> (keys | S) per bucket parity
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, tile_bound(n, chunks_per_bucket, T), stream),
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
     for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, lv, (int)n, sms, stream),
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
         ++launches;  // partition + merge
     }
@@ -408,14 +418,18 @@ hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtyp
     const long long nblocks = (n + TM - 1) / TM;
 
     Workspace ws;
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
+        return s;
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanChunks, T, stream), "K4 plan");
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, in, out, ws.S, tile_bound(n, chunks_per_bucket, T), stream), "K5 tile sort");
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, in, out, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
+                "K5 tile sort");
     const int L = level_bound(n, log2c, T, 1, 0);
     for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, lv, (int)n, sms, stream), "K6 merge level");
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
+                    "K6 merge level");
         ++launches;
     }
     return finish(ws, stream, launches);
@@ -450,9 +464,12 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
         g_err[0] = 0;
         return HS_OK;
     }
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, stream)) != HS_OK) return s;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) !=
+        HS_OK)
+        return s;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanMerge, 1, stream), "K4 plan");
+    HS_TRY_CUDA(hs::launch_sample(dt, in, ws.samp[0], n, sms, stream), "K6 sample");
     const void *src0 = in;
     if (in == out) {
         src0 = nullptr;
@@ -461,7 +478,9 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
         if (log2c & 1) HS_TRY_CUDA(hs::launch_copy(dt, in, ws.S, n, sms, stream), "K7 copy");
     }
     for (int lv = 0; lv < log2c; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, lv, (int)n, sms, stream), "K6 merge level");
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < log2c ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
+                    "K6 merge level");
         ++launches;
     }
     return finish(ws, stream, launches);

@@ -293,4 +293,41 @@ __device__ __forceinline__ void oddeven_sort(K (&v)[N]) {
     for (int c = 0; c < net.n; ++c) cas(v[net.a[c]], v[net.b[c]]);
 }
 
+
+// ------------------------------------------------------------ key samples
+// Every kernel that writes a generation of the sorted runs (the tile sort,
+// each merge level) also writes samp[p / kSampleQ] = key at position p for
+// every p = kSampleQ - 1 (mod kSampleQ).  The next merge level's co-rank
+// search runs its coarse phase on these samples (1/kSampleQ of the data,
+// stored with an L2 evict_last policy so they stay on chip while the level's
+// 2 n s bytes stream past) and touches HBM only for the last ~kSampleQ keys.
+constexpr int kSampleQ = 64;
+
+__device__ __forceinline__ void st_keep(int32_t *p, int32_t v) {
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "st.global.L2::cache_hint.b32 [%0], %1, pol;\n}" ::"l"(p),
+        "r"(v)
+        : "memory");
+}
+__device__ __forceinline__ void st_keep(int64_t *p, int64_t v) {
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p),
+        "l"(v)
+        : "memory");
+}
+
+// Write the samples of output positions [x, x + len) whose keys sit at
+// stage[p - x] (shared memory), threads tid = 0 .. nthreads-1 cooperating.
+template <typename K>
+__device__ __forceinline__ void write_samples(K *samp, long long x, int len, const K *stage, int tid, int nthreads) {
+    if (!samp) return;
+    const long long f = x + (kSampleQ - 1 - x % kSampleQ);  // first sample position >= x
+    for (long long p = f + (long long)tid * kSampleQ; p < x + len; p += (long long)nthreads * kSampleQ)
+        st_keep(samp + p / kSampleQ, stage[p - x]);
+}
+
 }  // namespace hs

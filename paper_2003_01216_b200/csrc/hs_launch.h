@@ -29,10 +29,14 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
                              int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
-cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
-                             cudaStream_t st);
-cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank, int level,
-                               int n, int num_sms, cudaStream_t st);
+cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
+                             long long max_tiles, cudaStream_t st);
+// samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
+// the samples this level writes for the next one (may be null).
+cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
+                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st);
+// samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
+cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);
 
 }  // namespace hs

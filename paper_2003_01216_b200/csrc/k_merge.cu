@@ -30,9 +30,6 @@
 #ifndef HS_MERGE_VT64
 #define HS_MERGE_VT64 13
 #endif
-#ifndef HS_PART_G
-#define HS_PART_G 1
-#endif
 #ifndef HS_MERGE_ST
 #define HS_MERGE_ST 2
 #endif
@@ -71,23 +68,22 @@ __device__ __forceinline__ void load_plan_m(Plan &dst, const Plan *src) {
 // Co-rank (merge-path) search for every TM-aligned output boundary of one
 // merge level: corank[beta] = absolute index into run A of the split of
 // output position beta*TM inside its pair (ties: A first, stable-left S:49).
-// G lanes cooperate on one boundary with a (G+1)-ary search: each round every
-// lane probes one candidate, a ballot finds the crossing, and the range
-// shrinks ~G+1 fold, so a 2^24-element pair takes ~6 rounds of parallel
-// probes instead of 24 dependent ones.
-template <typename K, int G>
-__global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0, int *corank, int level,
-                                  int n, int TM, int nbounds) {
-    static_assert(G >= 1 && G <= 32 && (32 % G) == 0, "group size");
+// Q(m) := A[m] <= B[diag-1-m] is true on a prefix of [l0, r0); the co-rank is
+// the first m where it fails.
+//   coarse: only at the m whose A[m] is a sample (position = Q-1 mod Q), with
+//     B[diag-1-m] bracketed by its two neighbouring B samples, Q(m) is either
+//     surely true, surely false or open; two binary searches over these
+//     candidates (samples only: L2-resident) leave an interval of ~Q keys;
+//   fine: plain binary search of Q(m) over that interval (the only HBM reads).
+template <typename K>
+__global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
+                                  const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds) {
+    constexpr long long Q = kSampleQ;
     __shared__ Plan P;
     load_plan_m(P, plan_g);
     __syncthreads();
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int beta = gtid / G;
-    const int j = gtid % G;
-    const int lane = threadIdx.x & 31;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - j));
-    // whole groups take the same path (beta, x, bucket are group-uniform)
+    if (level >= P.Lmax) return;  // no bucket runs this level (the host only knows a bound)
+    const int beta = blockIdx.x * blockDim.x + threadIdx.x;
     if (beta >= nbounds) return;
     const long long x = (long long)beta * TM;
     if (x >= n) return;
@@ -97,21 +93,52 @@ __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, c
     const K *src = (level == 0 && src0) ? src0 : level_src(P, b, level, F, S);
     const long long diag = x - g.a_lo;
     const long long na = g.b_lo - g.a_lo, nb = g.b_hi - g.b_lo;
-    long long l = diag - nb > 0 ? diag - nb : 0;  // answer in [l, r]; P(l) holds
+    long long l = diag - nb > 0 ? diag - nb : 0;  // answer in [l, r]
     long long r = diag < na ? diag : na;
-    const K *A = src + g.a_lo;
-    const K *B = src + g.b_lo;
-    while (l < r) {
-        const long long step = (r - l + G) / (G + 1);  // >= 1
-        const long long c = l + (long long)(j + 1) * step;
-        const bool p = (c <= r) && (A[c - 1] <= B[diag - c]);
-        const unsigned m = __ballot_sync(gmask, p) >> (lane - j);
-        const int cnt = __popc(m);  // probes are monotone: the true ones form a prefix
-        const long long fail = l + (long long)(cnt + 1) * step;  // first false probe (or past r)
-        l += (long long)cnt * step;
-        if (cnt < G && fail - 1 < r) r = fail - 1;  // a probe failed: the answer is below it
+    if (l < r) {
+        // candidates m_j = m0 + j Q, j < J, with A[m_j] a sample
+        const long long m0 = l + (Q - 1 - (g.a_lo + l) % Q);
+        const long long J = m0 < r ? (r - 1 - m0) / Q + 1 : 0;
+        // T(j): surely true (A[m_j] <= lower B sample), a prefix of j;
+        // F(j): surely false (A[m_j] > upper B sample), a suffix of j.
+        // Both binary searches advance together (independent L2 loads).
+        long long tlo = 0, thi = J, flo = 0, fhi = J;
+        while (tlo < thi || flo < fhi) {
+            const long long jt = (tlo + thi) >> 1, jf = (flo + fhi) >> 1;
+            const long long mt = m0 + jt * Q, mf = m0 + jf * Q;
+            const long long pl = (g.b_lo + diag - 1 - mt) / Q * Q - 1;
+            const long long pu = (g.b_lo + diag - 1 - mf) / Q * Q + Q - 1;
+            if (tlo < thi) {
+                const bool t = pl >= g.b_lo && __ldg(samp + (g.a_lo + mt) / Q) <= __ldg(samp + pl / Q);
+                if (t) tlo = jt + 1;
+                else thi = jt;
+            }
+            if (flo < fhi) {
+                const bool f = pu < g.b_hi && __ldg(samp + (g.a_lo + mf) / Q) > __ldg(samp + pu / Q);
+                if (f) fhi = jf;
+                else flo = jf + 1;
+            }
+        }
+        const long long jT = tlo, jF = flo;
+        if (jT > 0) l = m0 + (jT - 1) * Q + 1;
+        if (jF < J) r = m0 + jF * Q;
+        const K *A = src + g.a_lo;
+        const K *B = src + g.b_lo;
+        while (l < r) {
+            const long long mid = (l + r) >> 1;
+            if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
+            else r = mid;
+        }
     }
-    if (j == 0) corank[beta] = (int)(g.a_lo + l);
+    corank[beta] = (int)(g.a_lo + l);
+}
+
+// samp[m] = src[m Q + Q - 1]: the coarse index of caller-given runs (hs_merge).
+template <typename K>
+__global__ void k_sample(const K *__restrict__ src, K *samp, long long n) {
+    const long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long p = m * kSampleQ + kSampleQ - 1;
+    if (p < n) st_keep(samp + m, src[p]);
 }
 
 // =================================================================== K6b
@@ -164,8 +191,8 @@ __device__ __forceinline__ int merge_path(const K *A, int na, const K *B, int nb
 //             phase, one bulk async store of the aligned middle per piece.
 template <typename K, int NC, int VT, int ST>
 __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
-                                                         const int *__restrict__ corank, int level, int n,
-                                                         int nblocks) {
+                                                         const int *__restrict__ corank, K *samp_out, int level,
+                                                         int n, int nblocks) {
     using SM = MergeSmem<K, NC, VT, ST>;
     constexpr int TM = SM::TM, E = SM::E, SLOT = SM::SLOT, OUT = SM::OUT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -187,6 +214,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
         fence_mbar_init();
     }
     __syncthreads();
+    if (level >= P.Lmax) return;  // no bucket runs this level (the host only knows a bound)
 
     if (tid >= NC) {
         // ------------------------------------------------------ producer
@@ -355,6 +383,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
             for (int p = sh + tid; p < end; p += NC) g[p] = sOut[p];
         }
         if (tid == 0) bulk_commit();  // one group per piece (possibly empty)
+        write_samples(samp_out, q.x, q.len, sOut + sh, tid, NC);  // coarse index for the next level
     }
     if (tid == 0) bulk_wait0();
 }
@@ -373,8 +402,9 @@ int merge_span_t() {
 }
 
 template <typename K>
-cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void *src0, int *corank, int level, int n,
-                                 int num_sms, cudaStream_t st) {
+cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void *src0, int *corank,
+                                 const void *samp_in, void *samp_out, int level, int n, int num_sms,
+                                 cudaStream_t st) {
     using G = MGeo<K>;
     using SM = MergeSmem<K, G::kNT, G::kVT, G::kST>;
     constexpr int TM = SM::TM;
@@ -395,20 +425,28 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
     const int nbounds = nblocks + 1;
-    constexpr int PG = HS_PART_G;
-    const long long pthreads = (long long)nbounds * PG;
     prof_begin(kProfMergePartition, st);
-    k_merge_partition<K, PG><<<(unsigned)((pthreads + 255) / 256), 256, 0, st>>>(plan, (K *)F, (K *)S, (const K *)src0,
-                                                                               corank, level, n, TM, nbounds);
+    k_merge_partition<K><<<(unsigned)((nbounds + 127) / 128), 128, 0, st>>>(
+        plan, (K *)F, (K *)S, (const K *)src0, (const K *)samp_in, corank, level, n, TM, nbounds);
     prof_end(kProfMergePartition, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long grid = (long long)per_sm * num_sms;
     if (grid > nblocks) grid = nblocks;
     prof_begin(kProfMergeLevel, st);
-    kern<<<(unsigned)grid, G::kNT + 32, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank, level, n,
-                                                           nblocks);
+    kern<<<(unsigned)grid, G::kNT + 32, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank,
+                                                           (K *)samp_out, level, n, nblocks);
     prof_end(kProfMergeLevel, st);
+    return cudaGetLastError();
+}
+
+template <typename K>
+cudaError_t launch_sample_t(const void *src, void *samp, long long n, cudaStream_t st) {
+    const long long m = n / kSampleQ;
+    if (m <= 0) return cudaSuccess;
+    prof_begin(kProfMergePartition, st);
+    k_sample<K><<<(unsigned)((m + 255) / 256), 256, 0, st>>>((const K *)src, (K *)samp, n);
+    prof_end(kProfMergePartition, st);
     return cudaGetLastError();
 }
 
@@ -425,10 +463,15 @@ cudaError_t launch_copy_t(const void *src, void *dst, long long n, int num_sms, 
 
 int merge_span(int dt) { return dt == 0 ? merge_span_t<int32_t>() : merge_span_t<int64_t>(); }
 
-cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank, int level,
-                               int n, int num_sms, cudaStream_t st) {
-    return dt == 0 ? launch_merge_level_t<int32_t>(plan, F, S, src0, corank, level, n, num_sms, st)
-                   : launch_merge_level_t<int64_t>(plan, F, S, src0, corank, level, n, num_sms, st);
+cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
+                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st) {
+    return dt == 0 ? launch_merge_level_t<int32_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st)
+                   : launch_merge_level_t<int64_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st);
+}
+
+cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st) {
+    (void)num_sms;
+    return dt == 0 ? launch_sample_t<int32_t>(src, samp, n, st) : launch_sample_t<int64_t>(src, samp, n, st);
 }
 
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st) {

@@ -112,7 +112,8 @@ struct TSGeo {
 };
 
 template <typename K, int NT, int VT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S) {
+__global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
+                                                        K *samp) {
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     } else {
         for (int p = tid; p < len; p += NT) out[p] = so[p];
     }
+    write_samples(samp, lo, len, so, tid, NT);  // coarse index for merge level 0's co-rank search
 }
 
 // =============================================================== launchers
@@ -245,7 +247,7 @@ cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode
 }
 
 template <typename K>
-cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
+cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
                                cudaStream_t st) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
@@ -260,15 +262,15 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
-    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S);
+    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp);
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, long long max_tiles,
-                             cudaStream_t st) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, max_tiles, st)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, max_tiles, st);
+cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
+                             long long max_tiles, cudaStream_t st) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st);
 }
 
 }  // namespace hs

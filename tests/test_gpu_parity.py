@@ -232,7 +232,7 @@ def test_sort_chunk_counts(c):
     assert_same(host(d), O.sort(keys, 9, c), f"sort c={c}")
 
 
-@pytest.mark.parametrize("kind", ["equal", "sorted", "reversed", "two_values", "clamped", "negative"])
+@pytest.mark.parametrize("kind", ["equal", "sorted", "reversed", "two_values", "clamped", "negative", "int_max"])
 def test_sort_degenerate(kind):
     n = 3 * T32 * 8 + 123
     if kind == "equal":
@@ -245,6 +245,9 @@ def test_sort_degenerate(kind):
         keys = np.where(np.arange(n) % 3 == 0, 10, 999_999).astype(np.int32)
     elif kind == "clamped":   # keys >= 10^D and < 0 are clamped (reading #3); still a full sort
         keys = W.uniform(n, 3, 2**31 - 1, dtype=np.int32)
+    elif kind == "int_max":   # real keys equal to the dtype maximum (the tile sort's sentinel value)
+        keys = W.uniform(n, 5, 10**6, dtype=np.int32)
+        keys[::37] = np.iinfo(np.int32).max
     else:
         keys = (W.uniform(n, 4, 2**31 - 1, dtype=np.int32).astype(np.int64) - 2**30).astype(np.int32)
     d = dev(keys)
@@ -252,6 +255,17 @@ def test_sort_degenerate(kind):
     got = host(d)
     assert_same(got, O.sort(keys, 6, 8), kind)
     assert_same(got, np.sort(keys), kind + " (library special case)")
+
+
+def test_sort_int64_with_max_keys():
+    n = 5 * T64 * 8 + 77
+    keys = W.uniform(n, 6, 10**18, dtype=np.int64)
+    keys[::29] = np.iinfo(np.int64).max
+    d = dev(keys)
+    hs.hs_sort(d, 18, 8)
+    got = host(d)
+    assert_same(got, O.sort(keys, 18, 8), "int64 with INT64_MAX keys")
+    assert_same(got, np.sort(keys), "int64 with INT64_MAX keys (library special case)")
 
 
 def test_sort_worked_examples():
