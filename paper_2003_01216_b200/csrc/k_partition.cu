@@ -24,7 +24,7 @@
 #include "hs_launch.h"
 
 #ifndef HS_SCAT_NT
-#define HS_SCAT_NT 256
+#define HS_SCAT_NT 128
 #endif
 #ifndef HS_SCAT_VT
 #define HS_SCAT_VT 16
@@ -40,7 +40,7 @@ template <typename K>
 struct PGeo;
 template <>
 struct PGeo<int32_t> {
-    static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT;  // default 256 x 16 = 4096 keys per tile
+    static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT;  // default 128 x 16 = 2048 keys per tile
 };
 template <>
 struct PGeo<int64_t> {
