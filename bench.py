@@ -7,6 +7,11 @@ the BASELINE.json workload: C3 = 268,435,456 int32 keys uniform in [0, 1e9)
 (seed 3, D = 9, 8 chunks per bucket), keys resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+                  [--api sort|shared]
+
+--api shared times hs_sort_shared instead (the no-MSD
+ablation: chunk sort + tree merge of the whole array); --config P3 is
+the paper's own 3-digit workload (f4).
 
 N > 1 runs N independent replicas (one per GPU, launched by torchrun; the
 path does not shard -- DESIGN.md §7), timed as the max over ranks.
@@ -45,7 +50,8 @@ def peaks():
 
 
 def workload_desc(cfg):
-    kind = "uniform in [0, %d)" % cfg.value_range if cfg.kind == "uniform" else "70/20/10 normal/1024-value/uniform mixture"
+    kind = ("uniform in [%d, %d)" % (cfg.value_lo, cfg.value_lo + cfg.value_range) if cfg.kind == "uniform"
+            else "70/20/10 normal/1024-value/uniform mixture")
     return (f"{cfg.name}: {cfg.n:,} {cfg.dtype} keys, {kind}, seed {cfg.seed}, "
             f"D={cfg.num_digits} (MSD digit = floor(k/10^{cfg.num_digits - 1})), {cfg.chunks} chunks/bucket")
 
@@ -141,11 +147,16 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------------- ours
-def cpu_baseline(cfg, sample):
+def cpu_baseline(cfg, sample, shared=False):
     import oracle
     import workload as W
     keys = W.generate(cfg, 0, sample)
-    _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
+    if shared:
+        t0 = time.perf_counter()
+        oracle.sort_shared(keys, cfg.chunks)
+        dt, threads = time.perf_counter() - t0, 1
+    else:
+        _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
     return {"value": sample / dt / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": "oracle",
             "sample": f"first {sample:,} keys of {cfg.name} ({sample / cfg.n:.3g} of the workload), plain "
                       f"single-thread C oracle (gcc -O2), {dt:.2f} s for the sort call only"}
@@ -181,8 +192,13 @@ def run_ours(args, cfg):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    shared = args.api == "shared"
+
     def sort_step():
-        hs.hs_sort(buf, cfg.num_digits, cfg.chunks)
+        if shared:
+            hs.hs_sort_shared(buf, cfg.chunks)
+        else:
+            hs.hs_sort(buf, cfg.num_digits, cfg.chunks)
 
     def restore():
         buf.copy_(src)
@@ -232,8 +248,11 @@ def run_ours(args, cfg):
     prof = hs.profile_read()
     hs.profile_enable(False)
     # algorithmic bytes of the dominant kernel from the plan of this workload
-    _, off = hs.hs_msd_partition(src, cfg.num_digits)
-    off_h = off.cpu().numpy()
+    if shared:  # one segment: the whole array is "bucket 0"
+        off_h = np.array([0] + [cfg.n] * 10, dtype=np.int64)
+    else:
+        _, off = hs.hs_msd_partition(src, cfg.num_digits)
+        off_h = off.cpu().numpy()
     levels, tile_levels = hs.plan_levels(off_h, dt_code, cfg.chunks, 0)
     m = np.diff(off_h)
     per_kernel = {}
@@ -263,7 +282,8 @@ def run_ours(args, cfg):
                 "alg_bytes_per_launch": (statistics.mean(active) if dom == "merge_level" and active else alg.get(dom)),
                 "launches_per_step": per_kernel[dom]["launches_per_step"],
                 "active_launches_per_step": len(active) if dom == "merge_level" else 1}
-    path_bytes = ksize * cfg.n * 5 + sum(level_bytes)  # hist r + scatter r/w + tile sort r/w + levels
+    # hist r + scatter r/w (MSD path only) + tile sort r/w + merge levels
+    path_bytes = ksize * cfg.n * (2 if shared else 5) + sum(level_bytes)
     step_roof = {"alg_bytes_per_step": path_bytes, "t_roof_ms": path_bytes / (peak * 1e9) * 1e3,
                  "frac": path_bytes / (peak * 1e9) / (ms * 1e-3), "levels": max(levels)}
 
@@ -295,16 +315,17 @@ def run_ours(args, cfg):
                 f"{d.get('alg_GBps', 0):7.0f} GB/s alg")
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg, min(cfg.n, args.cpu_sample))
+            cpu = cpu_baseline(cfg, min(cfg.n, args.cpu_sample), shared)
             log(f"[bench] cpu_baseline {cpu}")
         line = {
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n_per_gpu": cfg.n, "num_digits": cfg.num_digits,
+                       "api": "hs_sort_shared (no MSD step, SURVEY f1)" if shared else "hs_sort",
                        "chunks_per_bucket": cfg.chunks, "merge_levels": max(levels),
                        "parallelism": "replicas" if world > 1 else "single GPU",
-                       "l2": "flushed (256 MiB device write) before every timed step; input 1 GiB > L2",
+                       "l2": "flushed (256 MiB device write) before every timed step",
                        "timing": "mean of per-step CUDA-event intervals around hs_sort on the launching stream; "
                                  "the untimed input restore + L2 flush sit between the intervals; max over ranks"},
             "roofline": roofline,
@@ -334,6 +355,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 26)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--api", default="sort", choices=["sort", "shared"])
     args = ap.parse_args()
     import workload as W
     cfg = W.CONFIGS[args.config]

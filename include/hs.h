@@ -142,6 +142,23 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
 hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                     cudaStream_t stream);
 
+/*
+ * SURVEY §8(f) row f1, the no-MSD ablation: the paper's Shared-Parallel
+ * Hybrid Quicksort + Merge Sort on the whole array (§3.2, "a hybrid
+ * algorithm ... Quicksort is used to sort the data assigned to each parallel
+ * thread ... then merged"; phases S:162-170), i.e. hs_sort without the MSD
+ * step: one segment of n keys is split by partition_even into
+ * `chunks` chunks, every chunk is sorted (tile sort + merge levels inside
+ * the chunk), then log2(chunks) tree-merge rounds merge them.
+ *
+ *   keys[n]            in/out: device; ascending on return.  In place.
+ *   chunks             power of two in [1, 65536] ("should be a power of
+ *                      two"), else HS_ERR_INVALID_VALUE.
+ * Errors as hs_sort.  The result equals hs_sort's (both are the unique
+ * ascending order of the keys).
+ */
+hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream);
+
 /* Static, human-readable name of a status code. */
 const char *hs_status_string(hs_status_t s);
 

@@ -69,6 +69,8 @@ def _lib(openmp: bool = False):
         lib.oracle_merge.restype = ci
         lib.oracle_sort.argtypes = [vp, i64, ci, i64, ci, ctypes.POINTER(i64)]
         lib.oracle_sort.restype = ci
+        lib.oracle_sort_shared.argtypes = [vp, i64, i64]
+        lib.oracle_sort_shared.restype = ci
         lib.oracle_openmp_threads.argtypes = []
         lib.oracle_openmp_threads.restype = ci
         _libs[key] = lib
@@ -174,6 +176,14 @@ def sort(keys, num_digits: int, chunks: int = 8, strict: bool = False, openmp: b
     k = _w(src)
     bad = ctypes.c_int64(-1)
     _check(_lib(openmp).oracle_sort(_p(k), k.size, num_digits, chunks, int(strict), ctypes.byref(bad)), bad.value)
+    return k.astype(src.dtype)
+
+
+def sort_shared(keys, chunks: int = 8, openmp: bool = False) -> np.ndarray:
+    """No-MSD ablation: chunk quicksort + tree merge of the whole array."""
+    src = np.asarray(keys)
+    k = _w(src)
+    _check(_lib(openmp).oracle_sort_shared(_p(k), k.size, chunks))
     return k.astype(src.dtype)
 
 

@@ -291,6 +291,23 @@ int oracle_sort(int64_t *keys, int64_t n, int num_digits, int64_t c, int strict,
     return rc;
 }
 
+/* ----------------------------------------------------------- f1 -------
+ * No-MSD ablation: the Shared-Parallel Hybrid Quicksort +
+ * Merge Sort of §3.2 on the whole array: the data is
+ * divided among c threads (partition_even, P:58 / S:138), each part is
+ * quicksorted (Fig 1c), then the parts are merged in a binary tree.
+ * Written as the one-segment case of the bucket routines above: a single
+ * "bucket" [0, n) (offsets 0, n, n, ..., n).                              */
+int oracle_sort_shared(int64_t *keys, int64_t n, int64_t c) {
+    if (!is_pow2(c)) return ORACLE_ERR_NOT_POW2;
+    int64_t off[11];
+    off[0] = 0;
+    for (int b = 1; b < 11; ++b) off[b] = n;
+    int rc = oracle_sort_chunks(keys, keys, n, off, c);
+    if (rc == ORACLE_OK) rc = oracle_merge(keys, keys, n, off, c);
+    return rc;
+}
+
 /* Reports whether this build runs the OpenMP pragmas (timing build). */
 int oracle_openmp_threads(void) {
 #ifdef _OPENMP

@@ -19,15 +19,15 @@ from . import _build
 
 __all__ = [
     "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
-    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_host",
-    "msd_partition", "sort_chunks", "merge", "sort", "sort_host",
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
+    "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS",
 ]
 
 HS_INT32, HS_INT64 = 0, 1
 STATUS = {0: "HS_OK", 1: "HS_ERR_INVALID_VALUE", 2: "HS_ERR_UNSUPPORTED_DTYPE", 3: "HS_ERR_OUT_OF_MEMORY", 4: "HS_ERR_CUDA"}
 EXPORTED_SYMBOLS = (
-    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_status_string",
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_status_string",
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels",
 )
@@ -62,7 +62,8 @@ def load(path: str | None = None):
     lib.hs_sort_chunks.argtypes = [vp, vp, i64, ci, vp, ci, vp]
     lib.hs_merge.argtypes = [vp, vp, i64, ci, vp, ci, vp]
     lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
-    for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort"):
+    lib.hs_sort_shared.argtypes = [vp, i64, ci, ci, vp]
+    for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared"):
         getattr(lib, f).restype = ci
     lib.hs_status_string.argtypes = [ci]
     lib.hs_status_string.restype = ctypes.c_char_p
@@ -239,6 +240,17 @@ def hs_sort(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None, vali
     return keys
 
 
+def hs_sort_shared(keys, chunks: int = 8, stream=None):
+    """No-MSD ablation: the paper's Shared-Parallel Hybrid
+    Quicksort + Merge Sort (§3.2) on the whole array, in place."""
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    dt = _dtype_code(keys)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort_shared(keys.data_ptr(), keys.numel(), dt, chunks, _stream(stream)))
+    return keys
+
+
 def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=None, out=None):
     """End-to-end convenience: pinned host keys -> H2D -> hs_sort -> D2H.
 
@@ -259,4 +271,5 @@ msd_partition = hs_msd_partition
 sort_chunks = hs_sort_chunks
 merge = hs_merge
 sort = hs_sort
+sort_shared = hs_sort_shared
 sort_host = hs_sort_host

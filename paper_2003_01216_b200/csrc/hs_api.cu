@@ -395,6 +395,42 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     return finish(ws, stream, launches - 1);
 }
 
+hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    const int dt = (int)dtype;
+    const int T = hs::sort_tile_keys(dt), TM = hs::merge_span(dt);
+    const long long nblocks = (n + TM - 1) / TM;
+    Workspace ws;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
+        return s;
+    int launches = 0;
+    const hs::Plan *plan = &ws.ctl->plan;
+    HS_TRY_CUDA(hs::launch_plan_whole(n, ws.ctl, log2c, T, stream), "K4 plan");
+    // chunk sort: leaf tiles keys -> (keys | S) by parity, in place per leaf
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, keys, keys, ws.S, ws.samp[0], tile_bound(n, chunks, T), stream),
+                "K5 tile sort");
+    const int L = level_bound(n, log2c, T, 1, 1);  // exact: the one segment is the whole array
+    for (int lv = 0; lv < L; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
+                    "K6 merge level");
+        ++launches;
+    }
+    return finish(ws, stream, launches);
+}
+
 hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
                            int chunks_per_bucket, cudaStream_t stream) {
     hs_status_t s;

@@ -29,6 +29,7 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
                              int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
+cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:

@@ -60,6 +60,16 @@ __global__ void k_plan(const long long *__restrict__ user_off, Ctl *ctl, int log
     }
 }
 
+// K4 for hs_sort_shared (no MSD step): the whole array is bucket 0.
+__global__ void k_plan_whole(Ctl *ctl, long long n, int log2c, int tile_keys) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        long long off[11];
+        off[0] = 0;
+        for (int b = 1; b < 11; ++b) off[b] = n;
+        compute_plan(&ctl->plan, off, log2c, kPlanSort, tile_keys);
+    }
+}
+
 // =================================================================== K5
 // Block merge sort of one leaf tile in shared memory.
 //   1. one 1-D bulk async copy (TMA engine) brings the leaf (a 16-byte aligned
@@ -242,6 +252,13 @@ int sort_tile_keys(int dt) {
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st) {
     prof_begin(kProfPlan, st);
     k_plan<<<1, 32, 0, st>>>(user_off, ctl, log2c, mode, tile_keys);
+    prof_end(kProfPlan, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st) {
+    prof_begin(kProfPlan, st);
+    k_plan_whole<<<1, 32, 0, st>>>(ctl, n, log2c, tile_keys);
     prof_end(kProfPlan, st);
     return cudaGetLastError();
 }

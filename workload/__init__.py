@@ -37,6 +37,7 @@ class Config:
     value_range: int    # uniform keys in [0, value_range)
     num_digits: int     # D: MSD digit = floor(k / 10^(D-1))
     chunks: int         # chunks per bucket (paper's threads per node)
+    value_lo: int = 0   # uniform keys are value_lo + [0, value_range)
 
 
 # BASELINE.json configs[0..4]; D per SURVEY §8(c) reading #2, c = 8 per reading #6.
@@ -46,6 +47,10 @@ CONFIGS = {
     "C3": Config("C3", 268_435_456, "int32", 3, "uniform", 10**9, 9, 8),
     "C4": Config("C4", 67_108_864, "int32", 4, "mixture", 10**9, 9, 8),
     "C5": Config("C5", 536_870_912, "int64", 5, "uniform", 10**18, 18, 8),
+    # SURVEY §8(f) f4, the paper's own workload: "each number consists of three
+    # digits", i.e. [100, 999], n up to 1e7; 900 distinct
+    # values, bucket 0 empty.  Not a BASELINE.json config.
+    "P3": Config("P3", 10_000_000, "int32", 6, "uniform", 900, 3, 8, value_lo=100),
 }
 
 
@@ -94,6 +99,8 @@ def generate(cfg: Config | str, start: int = 0, count: int | None = None, out: n
     if cfg.kind == "uniform":
         fn = lib.wl_uniform_i32 if cfg.dtype == "int32" else lib.wl_uniform_i64
         fn(_ptr(out), cfg.seed, cfg.value_range, start, count)
+        if cfg.value_lo:
+            out[:count] += cfg.value_lo
     else:
         assert cfg.dtype == "int32"
         lib.wl_mixture_i32(_ptr(out), cfg.seed, cfg.n, start, count)
@@ -163,7 +170,7 @@ def generate_np(cfg: Config | str, start: int = 0, count: int | None = None) -> 
     dt = np.int32 if cfg.dtype == "int32" else np.int64
     idx = np.arange(start, start + count, dtype=np.uint64)
     if cfg.kind == "uniform":
-        return mulhi_np(out_np(cfg.seed, idx), cfg.value_range).astype(dt)
+        return (mulhi_np(out_np(cfg.seed, idx), cfg.value_range).astype(np.int64) + cfg.value_lo).astype(dt)
     table = mulhi_np(out_np(cfg.seed, np.uint64(8 * cfg.n) + np.arange(1024, dtype=np.uint64)), 10**9).astype(np.int64)
     w = [out_np(cfg.seed, np.uint64(8) * idx + np.uint64(j)) for j in range(8)]
     sel = mulhi_np(w[0], 100)
