@@ -21,7 +21,7 @@ __all__ = [
     "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
-    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS",
+    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline",
 ]
 
 HS_INT32, HS_INT64 = 0, 1
@@ -265,6 +265,67 @@ def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=
     out.copy_(d, non_blocking=True)
     torch.cuda.current_stream(dev).synchronize()
     return out
+
+
+class HostSortPipeline:
+    """End-to-end sorting of a stream of host batches through hs_sort.
+
+    Each batch goes pinned host -> H2D -> hs_sort -> D2H.  Two device slots
+    and three CUDA streams (H2D copy, compute, D2H copy) let the H2D of batch
+    i+1 and the D2H of batch i-1 run on the copy engines while batch i is
+    sorted, so a long stream of batches is bounded by the slowest of the three
+    stages instead of their sum.  Ordering is kept with CUDA events only (no
+    host synchronisation except when a slot is reused and in ``finish``).
+
+        pipe = HostSortPipeline(n, torch.int32, num_digits=9, chunks=8)
+        for h_in, h_out in batches:      # pinned CPU tensors of n keys
+            pipe.submit(h_in, h_out)     # h_out holds the sorted keys once finish() returns
+        pipe.finish()
+    """
+
+    def __init__(self, n: int, dtype, num_digits: int, chunks: int = 8, device=None):
+        torch = _torch()
+        self.dev = torch.device(device or "cuda")
+        self.n, self.num_digits, self.chunks = n, num_digits, chunks
+        self.bufs = [torch.empty(n, dtype=dtype, device=self.dev) for _ in range(2)]
+        self.s_in = torch.cuda.Stream(self.dev)
+        self.s_cmp = torch.cuda.Stream(self.dev)
+        self.s_out = torch.cuda.Stream(self.dev)
+        self.out_done = [None, None]  # event: slot's D2H finished (slot free again)
+        self.i = 0
+
+    def submit(self, h_in, h_out) -> None:
+        torch = _torch()
+        slot = self.i & 1
+        buf = self.bufs[slot]
+        ev_free = self.out_done[slot]
+        with torch.cuda.stream(self.s_in):
+            if ev_free is not None:
+                self.s_in.wait_event(ev_free)
+            buf.copy_(h_in, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(self.s_in)
+        with torch.cuda.stream(self.s_cmp):
+            self.s_cmp.wait_event(ev_in)
+            hs_sort(buf, self.num_digits, self.chunks, stream=self.s_cmp)
+            ev_cmp = torch.cuda.Event()
+            ev_cmp.record(self.s_cmp)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(ev_cmp)
+            h_out.copy_(buf, non_blocking=True)
+            ev_out = torch.cuda.Event()
+            ev_out.record(self.s_out)
+        for t in (buf,):  # keep the caching allocator from recycling across streams
+            t.record_stream(self.s_in)
+            t.record_stream(self.s_cmp)
+            t.record_stream(self.s_out)
+        self.out_done[slot] = ev_out
+        self.i += 1
+
+    def finish(self) -> None:
+        for ev in self.out_done:
+            if ev is not None:
+                ev.synchronize()
 
 
 msd_partition = hs_msd_partition

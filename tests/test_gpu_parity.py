@@ -375,3 +375,17 @@ def test_merge_and_chunks_misaligned_views(dtype, shift):
     got = host(full)
     assert_same(got[shift:shift + n], O.merge(cs, off, 4), "merge in place")
     assert np.all(got[:shift] == 0) and np.all(got[shift + n:] == 0)
+
+
+def test_host_sort_pipeline():
+    """HostSortPipeline (public e2e API): every batch of a stream comes back sorted."""
+    n = 300_011
+    batches = [W.uniform(n, 300 + i, 10**9, dtype=np.int32) for i in range(5)]
+    h_in = [torch.from_numpy(b).pin_memory() for b in batches]
+    h_out = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in batches]
+    pipe = hs.HostSortPipeline(n, torch.int32, 9, 8, device=DEV)
+    for a, b in zip(h_in, h_out):
+        pipe.submit(a, b)
+    pipe.finish()
+    for i, b in enumerate(h_out):
+        assert_same(b.numpy(), O.sort(batches[i], 9, 8), f"pipeline batch {i}")
