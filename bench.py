@@ -376,6 +376,64 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_dist(args, cfg):
+    """the paper's cluster model over NCCL (weak scaling: every
+    rank holds cfg.n keys of its own; one all-to-all-v moves each digit group
+    to its owner rank, which sorts it).  Not the driver's default line."""
+    import torch
+    import torch.distributed as dist
+    import paper_2003_01216_b200 as hs
+    from paper_2003_01216_b200 import dist as hd
+    import workload as W
+
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29577")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", local)
+    hs.load()
+    tdt = torch.int32 if cfg.dtype == "int32" else torch.int64
+    h = torch.empty(cfg.n, dtype=tdt, pin_memory=True)
+    W.generate(cfg, rank * cfg.n, cfg.n, out=h.numpy())
+    src = h.to(dev)
+    buf = torch.empty_like(src)
+    times = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        buf.copy_(src)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out, info = hd.dist_sort(buf, cfg.num_digits, cfg.chunks)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            times.append(a.elapsed_time(b))
+    ms = statistics.mean(times)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = bool(torch.all(out[1:] >= out[:-1]).item()) if out.numel() > 1 else True
+    if rank == 0:
+        line = {"metric": METRIC, "value": world * cfg.n / (ms * 1e-3) / 1e9, "unit": "Gkeys/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+                "config": {"workload": workload_desc(cfg) + f" per rank (keys [rank*n, (rank+1)*n) of the stream)",
+                           "parallelism": f"bucket sharding over NCCL: {world} ranks (SURVEY f2, P:78-80)",
+                           "group_start": info.group_start, "max_group_keys": info.max_load,
+                           "timing": "CUDA events around dist_sort (partition, size all-gather, all-to-all-v, "
+                                     "local hs_sort), max over ranks"},
+                "sorted_check": ok}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -387,6 +445,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--api", default="sort", choices=["sort", "shared"])
+    ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
     args = ap.parse_args()
     import workload as W
     cfg = W.CONFIGS[args.config]
@@ -394,6 +453,8 @@ def main():
         if int(os.environ.get("RANK", "0")) != 0:
             return
         run_reference(args, cfg)
+    elif args.dist:
+        run_dist(args, cfg)
     else:
         run_ours(args, cfg)
 

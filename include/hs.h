@@ -159,6 +159,22 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
  */
 hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream);
 
+/*
+ * SURVEY §8(f) row f2, host side of the paper's cluster model (§3.4 Fig 4,
+ * P:80 "sends each bucket or buckets to proper node"
+ * assign_buckets): split the ten digits into `nodes` contiguous groups of at
+ * least one digit each, minimising the largest group total (exhaustive over
+ * all C(9, nodes-1) compositions); ties go to the lexicographically earliest
+ * sequence of split points.  Group g owns digits [group_start[g],
+ * group_start[g+1]).  Plain host code (no device, no stream).
+ *
+ *   bucket_sizes[10]   host int64 bucket totals (e.g. summed over ranks).
+ *   nodes              1 <= nodes <= 10, else HS_ERR_INVALID_VALUE.
+ *   group_start[nodes+1] host output: [0] = 0, [nodes] = 10.
+ *   max_load           host output (may be NULL): the minimised maximum.
+ */
+hs_status_t hs_assign_buckets(const int64_t *bucket_sizes, int nodes, int *group_start, int64_t *max_load);
+
 /* Static, human-readable name of a status code. */
 const char *hs_status_string(hs_status_t s);
 

@@ -29,7 +29,7 @@ STATUS = {0: "HS_OK", 1: "HS_ERR_INVALID_VALUE", 2: "HS_ERR_UNSUPPORTED_DTYPE", 
 EXPORTED_SYMBOLS = (
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_status_string",
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
-    "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels",
+    "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy")
 
@@ -81,6 +81,8 @@ def load(path: str | None = None):
     lib.hs_profile_kind_name.restype = ctypes.c_char_p
     lib.hs_plan_levels.argtypes = [vp, ci, ci, ci, vp, vp]
     lib.hs_plan_levels.restype = ci
+    lib.hs_assign_buckets.argtypes = [vp, ci, vp, vp]
+    lib.hs_assign_buckets.restype = ci
     if path is None:
         _LIB = lib
     return lib
@@ -130,6 +132,18 @@ def plan_levels(bucket_offsets_host, dtype_code: int, chunks: int, mode: int = 0
     if load().hs_plan_levels(off.ctypes.data, dtype_code, chunks, mode, L.ctypes.data, k.ctypes.data) < 0:
         raise ValueError("bad plan arguments")
     return L.tolist(), k.tolist()
+
+
+def assign_buckets(bucket_sizes, nodes: int):
+    """Contiguous digit groups for `nodes` nodes: (group_start[nodes+1], max_load)."""
+    import numpy as np
+    sizes = np.ascontiguousarray(np.asarray(bucket_sizes, dtype=np.int64))
+    if sizes.size != 10:
+        raise ValueError("bucket_sizes must have 10 entries")
+    gs = np.zeros(nodes + 1 if 1 <= nodes <= 10 else 1, dtype=np.int32)
+    ml = np.zeros(1, dtype=np.int64)
+    _check(load().hs_assign_buckets(sizes.ctypes.data, nodes, gs.ctypes.data, ml.ctypes.data))
+    return gs.tolist(), int(ml[0])
 
 
 # ------------------------------------------------------------ tensor glue

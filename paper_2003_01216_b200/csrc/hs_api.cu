@@ -290,6 +290,46 @@ int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chu
     return lmax;
 }
 
+hs_status_t hs_assign_buckets(const int64_t *bucket_sizes, int nodes, int *group_start, int64_t *max_load) {
+    if (!bucket_sizes || !group_start) return fail(HS_ERR_INVALID_VALUE, "NULL argument");
+    if (nodes < 1 || nodes > 10) return fail(HS_ERR_INVALID_VALUE, "nodes = %d outside [1, 10] (S:310)", nodes);
+    for (int d = 0; d < 10; ++d)
+        if (bucket_sizes[d] < 0) return fail(HS_ERR_INVALID_VALUE, "bucket_sizes[%d] < 0", d);
+    // Split points s_1 < ... < s_{m-1} in [1, 9], enumerated in lexicographic
+    // order (first ascending), so the first strict improvement found wins ties.
+    int cut[10], best[10];
+    long long best_load = -1;
+    const int m = nodes;
+    for (int i = 0; i < m - 1; ++i) cut[i] = i + 1;
+    for (;;) {
+        long long load = 0;
+        int lo = 0;
+        for (int g = 0; g < m; ++g) {
+            const int hi = g < m - 1 ? cut[g] : 10;
+            long long t = 0;
+            for (int d = lo; d < hi; ++d) t += bucket_sizes[d];
+            load = t > load ? t : load;
+            lo = hi;
+        }
+        if (best_load < 0 || load < best_load) {
+            best_load = load;
+            for (int i = 0; i < m - 1; ++i) best[i] = cut[i];
+        }
+        // next combination of m-1 cut positions out of 1..9
+        int i = m - 2;
+        while (i >= 0 && cut[i] == 9 - (m - 2 - i)) --i;
+        if (i < 0) break;
+        ++cut[i];
+        for (int j = i + 1; j < m - 1; ++j) cut[j] = cut[j - 1] + 1;
+    }
+    group_start[0] = 0;
+    for (int i = 0; i < m - 1; ++i) group_start[i + 1] = best[i];
+    group_start[m] = 10;
+    if (max_load) *max_load = best_load;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
 const char *hs_status_string(hs_status_t s) {
     switch (s) {
         case HS_OK: return "HS_OK";
