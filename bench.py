@@ -193,15 +193,25 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
 
     shared = args.api == "shared"
+    pairs = args.api == "pairs"
+    if pairs:
+        if cfg.dtype != "int32":
+            raise SystemExit("--api pairs needs an int32 config (f3 items are int32 keys + 64-bit tags)")
+        tags0 = torch.arange(cfg.n, dtype=torch.int64, device=dev)
+        tags = torch.empty_like(tags0)
 
     def sort_step():
         if shared:
             hs.hs_sort_shared(buf, cfg.chunks)
+        elif pairs:
+            hs.hs_sort_pairs(buf, tags, cfg.num_digits, cfg.chunks)
         else:
             hs.hs_sort(buf, cfg.num_digits, cfg.chunks)
 
     def restore():
         buf.copy_(src)
+        if pairs:
+            tags.copy_(tags0)
         flush.fill_(1)
 
     for _ in range(args.warmup):
@@ -253,7 +263,9 @@ def run_ours(args, cfg):
     else:
         _, off = hs.hs_msd_partition(src, cfg.num_digits)
         off_h = off.cpu().numpy()
-    levels, tile_levels = hs.plan_levels(off_h, dt_code, cfg.chunks, 0)
+    levels, tile_levels = hs.plan_levels(off_h, 1 if pairs else dt_code, cfg.chunks, 0)
+    if pairs:
+        ksize = 8  # the items (key << 32 | index) travel through the int64 path
     m = np.diff(off_h)
     per_kernel = {}
     for kind, (tot, cnt) in prof.items():
@@ -284,6 +296,8 @@ def run_ours(args, cfg):
                 "active_launches_per_step": len(active) if dom == "merge_level" else 1}
     # hist r + scatter r/w (MSD path only) + tile sort r/w + merge levels
     path_bytes = ksize * cfg.n * (2 if shared else 5) + sum(level_bytes)
+    if pairs:  # pack (r 4 + w 8), tag copy (r 8 + w 8), unpack (r 8 + tag gather 8 + w 4 + w 8)
+        path_bytes += cfg.n * (12 + 16 + 28)
     step_roof = {"alg_bytes_per_step": path_bytes, "t_roof_ms": path_bytes / (peak * 1e9) * 1e3,
                  "frac": path_bytes / (peak * 1e9) / (ms * 1e-3), "levels": max(levels)}
 
@@ -307,7 +321,7 @@ def run_ours(args, cfg):
     # pipelined stream of batches through the public HostSortPipeline (hs_sort
     # API only): H2D of step i+1 and D2H of step i-1 overlap the sort of step i
     e2e_pipe_ms = None
-    if not shared:
+    if not shared and not pairs:
         h_outs = [h_out, torch.empty_like(h_in, pin_memory=True)]
         pipe = hs.HostSortPipeline(cfg.n, tdt, cfg.num_digits, cfg.chunks, device=dev)
         for i in range(args.warmup):
@@ -346,7 +360,8 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n_per_gpu": cfg.n, "num_digits": cfg.num_digits,
-                       "api": "hs_sort_shared (no MSD step, SURVEY f1)" if shared else "hs_sort",
+                       "api": ("hs_sort_shared (no MSD step, SURVEY f1)" if shared else
+                               "hs_sort_pairs (int32 key + 64-bit tag items, stable; SURVEY f3)" if pairs else "hs_sort"),
                        "chunks_per_bucket": cfg.chunks, "merge_levels": max(levels),
                        "parallelism": "replicas" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB device write) before every timed step",
@@ -444,7 +459,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 26)
     ap.add_argument("--ref-sample", type=int, default=1 << 23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--api", default="sort", choices=["sort", "shared"])
+    ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
     args = ap.parse_args()
     import workload as W

@@ -160,6 +160,30 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
 hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream);
 
 /*
+ * SURVEY §8(f) row f3, the key + tag (stable) variant: SPEC's SortItem
+ * (a key plus a 64-bit tag that "never influences order"), sorted
+ * stably -- equal keys keep their input order, which the paper's merge sort
+ * guarantees ("Merge sort is a stable sort algorithm") and which the
+ * stable MSD scatter and the stable-left merge preserve.
+ * Keys are int32; the items travel through the int64 path as
+ * (key << 32) | input index, and the tags follow their index at the end.
+ *
+ * hs_msd_partition_pairs: a1-a3 on items.  keys[n] / tags[n] in (device);
+ *   out_keys[n] / out_tags[n] out (device, no overlap with the inputs);
+ *   bucket_offsets[11] as hs_msd_partition.  Within a bucket items keep their
+ *   input order.
+ * hs_sort_pairs: the whole path on items, in place: keys ascending, ties in
+ *   input order, tags permuted with their keys.
+ * n < 2^31; num_digits in [1, 10]; errors as hs_msd_partition / hs_sort.
+ * Scratch: 16 n bytes (items + one tag copy) on top of hs_sort's 8 n.
+ */
+hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, int64_t n, int num_digits,
+                                   int64_t *bucket_offsets, int32_t *out_keys, uint64_t *out_tags,
+                                   cudaStream_t stream);
+hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
+                          cudaStream_t stream);
+
+/*
  * SURVEY §8(f) row f2, host side of the paper's cluster model (§3.4 Fig 4,
  * P:80 "sends each bucket or buckets to proper node"
  * assign_buckets): split the ten digits into `nodes` contiguous groups of at

@@ -69,6 +69,10 @@ def _lib(openmp: bool = False):
         lib.oracle_merge.restype = ci
         lib.oracle_sort.argtypes = [vp, i64, ci, i64, ci, ctypes.POINTER(i64)]
         lib.oracle_sort.restype = ci
+        lib.oracle_msd_partition_pairs.argtypes = [vp, vp, i64, ci, vp, vp, vp]
+        lib.oracle_msd_partition_pairs.restype = ci
+        lib.oracle_sort_pairs.argtypes = [vp, vp, i64, ci, i64]
+        lib.oracle_sort_pairs.restype = ci
         lib.oracle_sort_shared.argtypes = [vp, i64, i64]
         lib.oracle_sort_shared.restype = ci
         lib.oracle_openmp_threads.argtypes = []
@@ -185,6 +189,27 @@ def sort_shared(keys, chunks: int = 8, openmp: bool = False) -> np.ndarray:
     k = _w(src)
     _check(_lib(openmp).oracle_sort_shared(_p(k), k.size, chunks))
     return k.astype(src.dtype)
+
+
+def msd_partition_pairs(keys, tags, num_digits: int):
+    """f3: stable MSD partition of (key, tag) items.  Returns (out_keys, out_tags, offsets11)."""
+    src = np.asarray(keys)
+    k = _w(src)
+    t = np.ascontiguousarray(np.asarray(tags).astype(np.uint64))
+    ok = np.empty_like(k)
+    ot = np.empty_like(t)
+    off = np.zeros(11, dtype=np.int64)
+    _check(_lib().oracle_msd_partition_pairs(_p(k), _p(t), k.size, num_digits, _p(off), _p(ok), _p(ot)))
+    return ok.astype(src.dtype), ot, off
+
+
+def sort_pairs(keys, tags, num_digits: int, chunks: int = 8):
+    """f3: stable sort of (key, tag) items: MSD partition -> Fig 1b merge sort per chunk -> tree merge."""
+    src = np.asarray(keys)
+    k = _w(src)
+    t = np.ascontiguousarray(np.asarray(tags).astype(np.uint64)).copy()
+    _check(_lib().oracle_sort_pairs(_p(k), _p(t), k.size, num_digits, chunks))
+    return k.astype(src.dtype), t
 
 
 def timed_sort(keys, num_digits: int, chunks: int = 8, openmp: bool = False):

@@ -308,6 +308,94 @@ int oracle_sort_shared(int64_t *keys, int64_t n, int64_t c) {
     return rc;
 }
 
+/* ----------------------------------------------------------- f3 -------
+ * Key + tag items (SPEC SortItem S:31-37: the tag never
+ * influences order), sorted STABLY: equal keys keep their input order.  The
+ * steps are the paper's, each in its stable form:
+ *   a1-a3  the MSD counting scatter (already stable), moving tags too;
+ *   a5     each chunk is sorted by the NON-recursive merge sort of Fig 1b
+ *          ("sort pairs, then repeatedly merge adjacent sorted
+ *          lists") -- the paper's stable sequential sort, used here
+ *          instead of quicksort (Fig 1c), which is not stable;
+ *   a6     the binary-tree merge of the chunks, stable-left.
+ * Keys are int64 (int32 callers widen), tags uint64.                      */
+static void merge_items(const int64_t *kl, const uint64_t *tl, int64_t nl, const int64_t *kr, const uint64_t *tr,
+                        int64_t nr, int64_t *ko, uint64_t *to) {
+    int64_t i = 0, j = 0, k = 0;
+    while (i < nl && j < nr) {
+        if (kr[j] < kl[i]) { ko[k] = kr[j]; to[k++] = tr[j++]; }
+        else { ko[k] = kl[i]; to[k++] = tl[i++]; }
+    }
+    while (i < nl) { ko[k] = kl[i]; to[k++] = tl[i++]; }
+    while (j < nr) { ko[k] = kr[j]; to[k++] = tr[j++]; }
+}
+
+/* Fig 1b: bottom-up merge sort of a[0..n) with tags, widths 1, 2, 4, ... */
+static void mergesort_items(int64_t *k, uint64_t *t, int64_t n, int64_t *kb, uint64_t *tb) {
+    for (int64_t w = 1; w < n; w *= 2) {
+        for (int64_t lo = 0; lo < n; lo += 2 * w) {
+            int64_t mid = lo + w < n ? lo + w : n, hi = lo + 2 * w < n ? lo + 2 * w : n;
+            merge_items(k + lo, t + lo, mid - lo, k + mid, t + mid, hi - mid, kb + lo, tb + lo);
+        }
+        memcpy(k, kb, (size_t)n * sizeof(int64_t));
+        memcpy(t, tb, (size_t)n * sizeof(uint64_t));
+    }
+}
+
+int oracle_msd_partition_pairs(const int64_t *keys, const uint64_t *tags, int64_t n, int num_digits,
+                               int64_t *offsets11, int64_t *out_keys, uint64_t *out_tags) {
+    int64_t cnt[10] = {0};
+    int d;
+    if (num_digits < 1 || num_digits > 19) return ORACLE_ERR_BAD_DIGITS;
+    for (int64_t i = 0; i < n; i++) {
+        oracle_digit(keys[i], num_digits, 0, &d);
+        cnt[d]++;
+    }
+    offsets11[0] = 0;
+    for (int b = 0; b < 10; b++) offsets11[b + 1] = offsets11[b] + cnt[b];
+    int64_t pos[10];
+    for (int b = 0; b < 10; b++) pos[b] = offsets11[b];
+    for (int64_t i = 0; i < n; i++) {
+        oracle_digit(keys[i], num_digits, 0, &d);
+        out_keys[pos[d]] = keys[i];
+        out_tags[pos[d]++] = tags[i];
+    }
+    return ORACLE_OK;
+}
+
+int oracle_sort_pairs(int64_t *keys, uint64_t *tags, int64_t n, int num_digits, int64_t c) {
+    if (!is_pow2(c)) return ORACLE_ERR_NOT_POW2;
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    int64_t *k1 = (int64_t *)malloc(nn * sizeof(int64_t)), *k2 = (int64_t *)malloc(nn * sizeof(int64_t));
+    uint64_t *t1 = (uint64_t *)malloc(nn * sizeof(uint64_t)), *t2 = (uint64_t *)malloc(nn * sizeof(uint64_t));
+    int64_t *lens = (int64_t *)malloc((size_t)c * sizeof(int64_t)), *starts = (int64_t *)malloc((size_t)(c + 1) * sizeof(int64_t));
+    int64_t *sched = (int64_t *)malloc((size_t)(3 * c + 3) * sizeof(int64_t));
+    int rc = ORACLE_OK;
+    if (!k1 || !k2 || !t1 || !t2 || !lens || !starts || !sched) rc = ORACLE_ERR_NOMEM;
+    int64_t off[11];
+    if (rc == ORACLE_OK) rc = oracle_msd_partition_pairs(keys, tags, n, num_digits, off, k1, t1);
+    for (int b = 0; rc == ORACLE_OK && b < 10; b++) {
+        chunk_starts(off[b], off[b + 1] - off[b], c, lens, starts);
+        for (int64_t i = 0; i < c; i++)   /* a5: stable sort of every chunk */
+            mergesort_items(k1 + starts[i], t1 + starts[i], lens[i], k2 + starts[i], t2 + starts[i]);
+        /* a6: round r merges chunk runs [i, i+2^(r-1)) and [i+2^(r-1), i+2^r) */
+        for (int64_t w = 1; w < c; w *= 2) {
+            for (int64_t i = 0; i < c; i += 2 * w) {
+                int64_t lo = starts[i], mid = starts[i + w], hi = starts[i + 2 * w];
+                merge_items(k1 + lo, t1 + lo, mid - lo, k1 + mid, t1 + mid, hi - mid, k2 + lo, t2 + lo);
+                memcpy(k1 + lo, k2 + lo, (size_t)(hi - lo) * sizeof(int64_t));
+                memcpy(t1 + lo, t2 + lo, (size_t)(hi - lo) * sizeof(uint64_t));
+            }
+        }
+    }
+    if (rc == ORACLE_OK) {
+        memcpy(keys, k1, (size_t)n * sizeof(int64_t));
+        memcpy(tags, t1, (size_t)n * sizeof(uint64_t));
+    }
+    free(k1); free(k2); free(t1); free(t2); free(lens); free(starts); free(sched);
+    return rc;
+}
+
 /* Reports whether this build runs the OpenMP pragmas (timing build). */
 int oracle_openmp_threads(void) {
 #ifdef _OPENMP

@@ -21,6 +21,7 @@ __all__ = [
     "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
+    "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
     "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline",
 ]
 
@@ -30,6 +31,7 @@ EXPORTED_SYMBOLS = (
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_status_string",
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
+    "hs_msd_partition_pairs", "hs_sort_pairs",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy")
 
@@ -63,7 +65,10 @@ def load(path: str | None = None):
     lib.hs_merge.argtypes = [vp, vp, i64, ci, vp, ci, vp]
     lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
     lib.hs_sort_shared.argtypes = [vp, i64, ci, ci, vp]
-    for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared"):
+    lib.hs_msd_partition_pairs.argtypes = [vp, vp, i64, ci, vp, vp, vp, vp]
+    lib.hs_sort_pairs.argtypes = [vp, vp, i64, ci, ci, vp]
+    for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared",
+              "hs_msd_partition_pairs", "hs_sort_pairs"):
         getattr(lib, f).restype = ci
     lib.hs_status_string.argtypes = [ci]
     lib.hs_status_string.restype = ctypes.c_char_p
@@ -265,6 +270,39 @@ def hs_sort_shared(keys, chunks: int = 8, stream=None):
     return keys
 
 
+def _check_pairs(keys, tags):
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    _check_tensor(tags, "tags")
+    if keys.dtype != torch.int32:
+        raise TypeError("hs_*_pairs: keys must be torch.int32")
+    if tags.element_size() != 8 or tags.numel() != keys.numel():
+        raise ValueError("tags must be a 64-bit tensor with one tag per key")
+
+
+def hs_msd_partition_pairs(keys, tags, num_digits: int, stream=None):
+    """f3: stable MSD partition of (key, tag) items.  Returns (out_keys, out_tags, bucket_offsets)."""
+    torch = _torch()
+    _check_pairs(keys, tags)
+    out_k = torch.empty_like(keys)
+    out_t = torch.empty_like(tags)
+    off = torch.empty(11, dtype=torch.int64, device=keys.device)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_msd_partition_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits,
+                                             off.data_ptr(), out_k.data_ptr(), out_t.data_ptr(), _stream(stream)))
+    return out_k, out_t, off
+
+
+def hs_sort_pairs(keys, tags, num_digits: int, chunks_per_bucket: int = 8, stream=None):
+    """f3: stable sort of (key, tag) items in place (ties keep input order).  Returns (keys, tags)."""
+    torch = _torch()
+    _check_pairs(keys, tags)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, chunks_per_bucket,
+                                    _stream(stream)))
+    return keys, tags
+
+
 def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=None, out=None):
     """End-to-end convenience: pinned host keys -> H2D -> hs_sort -> D2H.
 
@@ -347,4 +385,6 @@ sort_chunks = hs_sort_chunks
 merge = hs_merge
 sort = hs_sort
 sort_shared = hs_sort_shared
+sort_pairs = hs_sort_pairs
+msd_partition_pairs = hs_msd_partition_pairs
 sort_host = hs_sort_host

@@ -351,17 +351,14 @@ int hs_tile_keys(hs_dtype_t dtype, int which) {
     return which == 0 ? hs::scatter_tile_keys(dt) : which == 1 ? hs::sort_tile_keys(dt) : hs::merge_span(dt);
 }
 
-hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int64_t *bucket_offsets,
-                             void *out, cudaStream_t stream) {
+}  // extern "C"
+
+namespace {
+
+// a1-a3 on validated arguments.  key_shift: int64 items whose key is k >> 32.
+hs_status_t partition_impl(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift,
+                           int64_t *bucket_offsets, void *out, cudaStream_t stream, int *launches_out) {
     hs_status_t s;
-    if ((s = check_common(n, dtype)) != HS_OK) return s;
-    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
-    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
-    if ((s = check_ptr(out, n, dtype, "out")) != HS_OK) return s;
-    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
-    if (((uintptr_t)bucket_offsets & 7) != 0) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is not 8-byte aligned");
-    if (n > 0 && overlap(keys, out, (size_t)n * ksize(dtype)))
-        return fail(HS_ERR_INVALID_VALUE, "keys and out overlap (the partition is out of place)");
     int sms;
     cudaError_t e = device_setup(&sms);
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
@@ -378,11 +375,90 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
     int launches = 0;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
     HS_TRY_CUDA(hs::launch_partition(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status,
-                                     (long long *)bucket_offsets, -1, 0, 0, sms, true, stream),
+                                     (long long *)bucket_offsets, -1, 0, 0, sms, true, stream, key_shift),
                 "K1-K3 partition");
     launches += (tiles > 0 ? 2 : 0);  // K1, K2, K3 (K1/K3 skipped when n = 0)
-    return finish(ws, stream, launches - 1);  // the memset is not one of our kernels
+    cudaError_t fe = cudaFreeAsync(ws.base, stream);
+    if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    *launches_out = launches - 1;  // the memset is not one of our kernels
+    return HS_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int64_t *bucket_offsets,
+                             void *out, cudaStream_t stream) {
+    hs_status_t s;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if ((s = check_ptr(out, n, dtype, "out")) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if (((uintptr_t)bucket_offsets & 7) != 0) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is not 8-byte aligned");
+    if (n > 0 && overlap(keys, out, (size_t)n * ksize(dtype)))
+        return fail(HS_ERR_INVALID_VALUE, "keys and out overlap (the partition is out of place)");
+    int launches = 0;
+    if ((s = partition_impl(keys, n, dtype, num_digits, 0, bucket_offsets, out, stream, &launches)) != HS_OK) return s;
+    g_launches = launches;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// a1-a7 on validated arguments (n > 0).  key_shift as partition_impl.
+hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
+                      int log2c, cudaStream_t stream, int *launches_out) {
+    hs_status_t s;
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+
+    const int dt = (int)dtype;
+    const int Tp = hs::scatter_tile_keys(dt), T = hs::sort_tile_keys(dt), TM = hs::merge_span(dt);
+    const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
+    const long long ptiles = (n + h + Tp - 1) / Tp;
+    const long long nblocks = (n + TM - 1) / TM;
+    unsigned long long div, magic;
+    digit_params(num_digits, key_shift ? HS_INT64 : dtype, &div, &magic);
+
+    Workspace ws;
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
+                      (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
+        return s;
+    int launches = 0;
+    const hs::Plan *plan = &ws.ctl->plan;
+    HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
+    // a1-a3: tile histograms, lookback prefix (+ offsets + plan), stable scatter keys -> S
+    HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                     ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift),
+                "K1-K3 partition");
+    launches += 2;
+    // a5: leaf-tile sort S -> (keys | S) per bucket parity
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
+                "K5 tile sort");
+    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
+    const int L = level_bound(n, log2c, T, 1, 1);
+    for (int lv = 0; lv < L; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
+                    "K6 merge level");
+        ++launches;  // partition + merge
+    }
+    cudaError_t fe = cudaFreeAsync(ws.base, stream);
+    if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    *launches_out = launches - 1;  // the memset is not one of our kernels
+    return HS_OK;
+}
+
+
+}  // namespace
+
+extern "C" {
 
 hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                     cudaStream_t stream) {
@@ -397,42 +473,102 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
         g_err[0] = 0;
         return HS_OK;
     }
+    int launches = 0;
+    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) return s;
+    g_launches = launches;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, int64_t n, int num_digits,
+                                   int64_t *bucket_offsets, int32_t *out_keys, uint64_t *out_tags,
+                                   cudaStream_t stream) {
+    hs_status_t s;
+    if ((s = check_common(n, HS_INT32)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, HS_INT32)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, HS_INT32, "keys")) != HS_OK) return s;
+    if ((s = check_ptr(out_keys, n, HS_INT32, "out_keys")) != HS_OK) return s;
+    if ((s = check_ptr(tags, n, HS_INT64, "tags")) != HS_OK) return s;
+    if ((s = check_ptr(out_tags, n, HS_INT64, "out_tags")) != HS_OK) return s;
+    if (!bucket_offsets || ((uintptr_t)bucket_offsets & 7) != 0)
+        return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL or not 8-byte aligned");
+    if (n > 0 && (overlap(keys, out_keys, (size_t)n * 4) || overlap(tags, out_tags, (size_t)n * 8)))
+        return fail(HS_ERR_INVALID_VALUE, "inputs and outputs overlap (the partition is out of place)");
     int sms;
     cudaError_t e = device_setup(&sms);
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
-
-    const int dt = (int)dtype;
-    const int Tp = hs::scatter_tile_keys(dt), T = hs::sort_tile_keys(dt), TM = hs::merge_span(dt);
-    const int h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
-    const long long ptiles = (n + h + Tp - 1) / Tp;
-    const long long nblocks = (n + TM - 1) / TM;
-    unsigned long long div, magic;
-    digit_params(num_digits, dtype, &div, &magic);
-
-    Workspace ws;
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
-                      (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
-        return s;
-    int launches = 0;
-    const hs::Plan *plan = &ws.ctl->plan;
-    HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
-    // a1-a3: tile histograms, lookback prefix (+ offsets + plan), stable scatter keys -> S
-    HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
-                                     ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream),
-                "K1-K3 partition");
-    launches += 2;
-    // a5: leaf-tile sort S -> (keys | S) per bucket parity
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
-                "K5 tile sort");
-    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
-    const int L = level_bound(n, log2c, T, 1, 1);
-    for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
-                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
-                    "K6 merge level");
-        ++launches;  // partition + merge
+    void *buf = nullptr;
+    const size_t ib = (size_t)(n > 0 ? n : 1) * 8;
+    if ((e = cudaMallocAsync(&buf, 2 * ib + 256, stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed", 2 * ib + 256);
     }
-    return finish(ws, stream, launches - 1);
+    long long *items = (long long *)buf, *parted = (long long *)((char *)buf + round_up(ib, 256));
+    int launches = 0;
+    if ((e = hs::launch_pack_items(keys, items, n, sms, stream)) != cudaSuccess) {
+        cudaFreeAsync(buf, stream);
+        return cuda_fail(e, "K0 pack items");
+    }
+    if ((s = partition_impl(items, n, HS_INT64, num_digits, 32, bucket_offsets, parted, stream, &launches)) != HS_OK) {
+        cudaFreeAsync(buf, stream);
+        return s;
+    }
+    if ((e = hs::launch_unpack_items(parted, out_keys, (const unsigned long long *)tags,
+                                     (unsigned long long *)out_tags, n, sms, stream)) != cudaSuccess) {
+        cudaFreeAsync(buf, stream);
+        return cuda_fail(e, "K8 unpack items");
+    }
+    if ((e = cudaFreeAsync(buf, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    g_launches = launches + (n > 0 ? 2 : 0);
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
+                          cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, HS_INT32)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, HS_INT32)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, HS_INT32, "keys")) != HS_OK) return s;
+    if ((s = check_ptr(tags, n, HS_INT64, "tags")) != HS_OK) return s;
+    if (n > 0 && overlap(keys, tags, (size_t)n * 4)) return fail(HS_ERR_INVALID_VALUE, "keys and tags overlap");
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    void *buf = nullptr;
+    const size_t ib = round_up((size_t)n * 8, 256);
+    if ((e = cudaMallocAsync(&buf, 2 * ib, stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed", 2 * ib);
+    }
+    long long *items = (long long *)buf;
+    unsigned long long *tag_copy = (unsigned long long *)((char *)buf + ib);
+    int launches = 0;
+    if ((e = hs::launch_pack_items(keys, items, n, sms, stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(tag_copy, tags, (size_t)n * 8, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess) {
+        cudaFreeAsync(buf, stream);
+        return cuda_fail(e, "K0 pack items / tag copy");
+    }
+    if ((s = sort_impl(items, n, HS_INT64, num_digits, 32, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) {
+        cudaFreeAsync(buf, stream);
+        return s;
+    }
+    if ((e = hs::launch_unpack_items(items, keys, tag_copy, (unsigned long long *)tags, n, sms, stream)) !=
+        cudaSuccess) {
+        cudaFreeAsync(buf, stream);
+        return cuda_fail(e, "K8 unpack items");
+    }
+    if ((e = cudaFreeAsync(buf, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    g_launches = launches + 2;
+    g_err[0] = 0;
+    return HS_OK;
 }
 
 hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream) {

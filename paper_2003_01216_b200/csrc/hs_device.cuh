@@ -34,6 +34,7 @@ template <typename K>
 struct DigitParams {
     typename KeyTraits<K>::U div;
     typename KeyTraits<K>::U magic;
+    int shift;  // int64 only: the key is k >> shift (32 for the (key << 32 | index) items of hs_sort_pairs)
 };
 
 __device__ __forceinline__ int msd_digit(int32_t k, const DigitParams<int32_t> &p) {
@@ -46,6 +47,7 @@ __device__ __forceinline__ int msd_digit(int32_t k, const DigitParams<int32_t> &
 }
 
 __device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &p) {
+    k >>= p.shift;  // arithmetic: keeps the sign of the key
     if (k < 0) return 0;
     unsigned long long u = (unsigned long long)k;
     unsigned long long q = __umul64hi(u, p.magic);

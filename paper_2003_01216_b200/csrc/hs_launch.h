@@ -27,7 +27,8 @@ int scan_ctas(long long ntiles);
 cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, unsigned long long div,
                              unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
-                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st);
+                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st,
+                             int key_shift = 0);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
@@ -39,5 +40,10 @@ cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const
 // samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);
+
+// f3 key + tag items (k_pairs.cu)
+cudaError_t launch_pack_items(const int32_t *keys, long long *items, long long n, int num_sms, cudaStream_t st);
+cudaError_t launch_unpack_items(const long long *items, int32_t *keys, const unsigned long long *tag_in,
+                                unsigned long long *tag_out, long long n, int num_sms, cudaStream_t st);
 
 }  // namespace hs

@@ -450,12 +450,13 @@ template <typename K>
 cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsigned long long div,
                                unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                                unsigned long long *status, long long *user_off, int plan_mode, int log2c,
-                               int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st) {
+                               int sort_tile_keys, int num_sms, bool do_scatter, int key_shift, cudaStream_t st) {
     using G = PGeo<K>;
     constexpr int TP = G::kScatNT * G::kScatVT;
     DigitParams<K> dp;
     dp.div = (typename KeyTraits<K>::U)div;
     dp.magic = (typename KeyTraits<K>::U)magic;
+    dp.shift = key_shift;
     const long long ntiles = ((long long)n + h + TP - 1) / TP;
     if (ntiles > 0) {
         long long want = (ntiles + kHistWarps - 1) / kHistWarps;
@@ -508,11 +509,12 @@ int scan_ctas(long long ntiles) {
 cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, unsigned long long div,
                              unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
-                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st) {
+                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st, int key_shift) {
     return dt == 0 ? launch_partition_t<int32_t>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status,
-                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, st)
+                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, 0, st)
                    : launch_partition_t<int64_t>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status,
-                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, st);
+                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter,
+                                                 key_shift, st);
 }
 
 }  // namespace hs

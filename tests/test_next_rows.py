@@ -2,6 +2,10 @@
 
 f1  No-MSD ablation: ``hs_sort_shared`` = the paper's
     Shared-Parallel Hybrid Quicksort + Merge Sort on the whole array.
+f3  Key + tag items, sorted stably (SPEC SortItem S:31-37; "merge sort
+    is a stable sort"): ``hs_sort_pairs`` / ``hs_msd_partition_pairs`` against
+    the oracle's stable path (Fig 1b merge sort per chunk) -- the tie order is
+    observable through the tags.
 f4  The paper's own workload: config P3, 10^7 three-digit keys
     in [100, 999] -- 900 distinct values, bucket 0 empty.
 
@@ -135,3 +139,82 @@ def test_p3_full_bitexact():
     assert np.array_equal(off.cpu().numpy(), ref_off) and np.array_equal(out.cpu().numpy(), ref_out)
     assert int(ref_off[1]) == 0  # bucket 0 empty
     assert np.array_equal(_run_shared(keys, 8), O.sort_shared(keys, 8))
+
+
+# ------------------------------------------------------ f3: key + tag items
+def stable_ref(keys, tags):
+    """Python's sorted() is stable: the unique stable order of (key, tag) items by key."""
+    items = sorted(zip(np.asarray(keys).tolist(), np.asarray(tags).tolist()), key=lambda kv: kv[0])
+    return (np.array([k for k, _ in items], dtype=np.asarray(keys).dtype),
+            np.array([t for _, t in items], dtype=np.uint64))
+
+
+def test_sort_pairs_oracle_bruteforce():
+    for _ in range(300):
+        n = int(rng.integers(0, 300))
+        c = int(2 ** rng.integers(0, 5))
+        keys = rng.integers(0, 40, size=n).astype(np.int32)       # many ties
+        tags = rng.permutation(n).astype(np.uint64)
+        k, t = O.sort_pairs(keys, tags, 2, c)
+        rk, rt = stable_ref(keys, tags)
+        assert np.array_equal(k, rk) and np.array_equal(t, rt)
+
+
+def test_sort_pairs_oracle_npsort_stable_and_partition():
+    keys = W.generate("C4")[:400_000]                             # heavy duplicates (1024-value table)
+    tags = np.arange(keys.size, dtype=np.uint64)
+    k, t = O.sort_pairs(keys, tags, 9, 8)
+    order = np.argsort(keys, kind="stable")                        # library stable sort
+    assert np.array_equal(k, keys[order]) and np.array_equal(t, tags[order])
+    pk, pt, off = O.msd_partition_pairs(keys, tags, 9)
+    d = np.clip(keys.astype(np.int64) // 10**8, 0, 9)
+    order = np.argsort(d, kind="stable")
+    assert np.array_equal(pk, keys[order]) and np.array_equal(pt, tags[order])
+    assert np.array_equal(off, np.concatenate([[0], np.cumsum(np.bincount(d, minlength=10))]))
+
+
+def _run_pairs(keys, tags, D, c):
+    torch, hs = _gpu()
+    dk = torch.from_numpy(np.ascontiguousarray(keys)).to("cuda:0")
+    dt = torch.from_numpy(np.ascontiguousarray(tags).view(np.int64)).to("cuda:0")
+    hs.hs_sort_pairs(dk, dt, D, c)
+    torch.cuda.synchronize()
+    return dk.cpu().numpy(), dt.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n", [("C1", None), ("C4", 3_000_000), ("P3", 2_000_000)])
+def test_sort_pairs_parity(name, n):
+    cfg = W.CONFIGS[name]
+    keys = W.generate(name, 0, n)
+    tags = W.uniform(keys.size, 77, 2**62, dtype=np.int64).astype(np.uint64)
+    k, t = _run_pairs(keys, tags, cfg.num_digits, 8)
+    rk, rt = O.sort_pairs(keys, tags, cfg.num_digits, 8)
+    assert np.array_equal(k, rk)
+    assert np.array_equal(t, rt)    # ties in input order: only a stable path matches
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 5, 13_825, 100_003])
+def test_sort_pairs_edges(n):
+    keys = W.uniform(n, 91, 2**31 - 1, dtype=np.int32) - 2**30    # negative and clamped keys
+    if n > 3:
+        keys[::3] = np.iinfo(np.int32).max
+        keys[1::7] = np.iinfo(np.int32).min
+    tags = np.arange(n, dtype=np.uint64) * 3 + 1
+    k, t = _run_pairs(keys, tags, 6, 4)
+    rk, rt = stable_ref(keys, tags)
+    assert np.array_equal(k, rk) and np.array_equal(t, rt)
+
+
+@pytest.mark.gpu
+def test_msd_partition_pairs_parity():
+    torch, hs = _gpu()
+    keys = W.generate("C4", 0, 1_000_003)
+    tags = np.arange(keys.size, dtype=np.uint64)[::-1].copy()
+    ok, ot, off = hs.hs_msd_partition_pairs(torch.from_numpy(keys).cuda(),
+                                            torch.from_numpy(tags.view(np.int64)).cuda(), 9)
+    rk, rt, roff = O.msd_partition_pairs(keys, tags, 9)
+    assert np.array_equal(off.cpu().numpy(), roff)
+    assert np.array_equal(ok.cpu().numpy(), rk)
+    assert np.array_equal(ot.cpu().numpy().view(np.uint64), rt)
