@@ -114,6 +114,21 @@ __device__ __forceinline__ int smem_merge_path(const K *sm, int a0, int na, int 
     return l;
 }
 
+template <typename K>
+__device__ __forceinline__ K lds_k(uint32_t a);
+template <>
+__device__ __forceinline__ int32_t lds_k<int32_t>(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+template <>
+__device__ __forceinline__ int64_t lds_k<int64_t>(uint32_t a) {
+    int64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+
 template <typename K, int NT, int VT>
 struct TSGeo {
     static constexpr int T = NT * VT;
@@ -170,38 +185,58 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
     if (live0) oddeven_sort<VT>(v);
 
-    // 3. merge rounds (R = threads per run)
+    // 3. merge rounds (R = threads per run).  Bitonic storage: in round R the
+    // input run q (length RL = R VT) is stored ascending if q is even (the
+    // pair's A) and DESCENDING if q is odd (the pair's B), so a pair occupies
+    // one bitonic stretch of shared memory.  A thread merges from both ends
+    // of what is left of it: the smaller of the two end keys is always the
+    // next output, even after one run is exhausted (the pointers then walk
+    // towards each other inside the other run), so the serial merge needs no
+    // bounds tests and no sentinels; ties take the A end (stable-left).
+    // Every thread stores every round (threads past the leaf's end hold
+    // kMax pads), so the stretch is complete; only threads with an output
+    // below len merge.
+    const uint32_t sm_u = smem_u32(sm);
 #pragma unroll 1
-    for (int R = 1; R < NT; R <<= 1) {
-        const bool live = tid * VT < len;
-        __syncthreads();  // everyone has read the previous round's runs
-        if (live) {
+    for (int lgR = 0; (1 << lgR) < NT; ++lgR) {
+        const int R = 1 << lgR, RL = R * VT;
+        const int q = tid >> lgR;  // this thread's outputs form part of input run q
+        __syncthreads();           // everyone has read the previous round's runs
+        if ((q & 1) == 0) {
 #pragma unroll
             for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
+        } else {  // run q reversed in place: canonical c <-> (2q+1) RL - 1 - c
+            const int m = (2 * q + 1) * RL - 1 - tid * VT;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) sm[m - k] = v[k];
         }
         __syncthreads();
-        if (live) {
+        if (tid * VT < len) {
             const int j = tid & (2 * R - 1);
-            const int a0 = (tid - j) * VT, run = R * VT, b0 = a0 + run;
+            const int a0 = (tid - j) * VT, bE = a0 + 2 * RL;  // A = sm[a0, a0+RL) asc, B[k] = sm[bE-1-k]
             const int diag = j * VT;
-            const int s = smem_merge_path(sm, a0, run, b0, run, diag);
-            const int a_end = b0, b_end = b0 + run;
-            int ai = a0 + s, bi = b0 + diag - s;
-            K x = ai < a_end ? sm[ai] : kMax;
-            K y = bi < b_end ? sm[bi] : kMax;
+            // merge path: first m with !(A[m] <= B[diag-1-m]); B[diag-1-m] = sm[bE - diag + m]
+            int l = diag - RL > 0 ? diag - RL : 0, r = diag < RL ? diag : RL;
+            const uint32_t ua = sm_u + (uint32_t)a0 * sizeof(K), ub = sm_u + (uint32_t)(bE - diag) * sizeof(K);
+            while (l < r) {
+                const int mid = (l + r) >> 1;
+                const bool pr = lds_k<K>(ua + mid * (int)sizeof(K)) <= lds_k<K>(ub + mid * (int)sizeof(K));
+                l = pr ? mid + 1 : l;
+                r = pr ? r : mid;
+            }
+            uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
+            uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
+            K x = lds_k<K>(pi), y = lds_k<K>(pj);
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
                 const bool p = x <= y;
                 v[k] = p ? x : y;
                 if (k + 1 < VT) {
-                    const int nx = (p ? ai : bi) + 1;
-                    const int lim = p ? a_end : b_end;
-                    const K t = sm[nx];  // nx <= T: inside the buffer (T + 2E slots)
-                    const K tv = nx < lim ? t : kMax;
-                    ai = p ? nx : ai;
-                    bi = p ? bi : nx;
-                    x = p ? tv : x;
-                    y = p ? y : tv;
+                    pi += p ? (uint32_t)sizeof(K) : 0u;
+                    pj -= p ? 0u : (uint32_t)sizeof(K);
+                    const K t = lds_k<K>(p ? pi : pj);
+                    x = p ? t : x;
+                    y = p ? y : t;
                 }
             }
         }
