@@ -288,11 +288,34 @@ struct OddEvenNet {
     }
 };
 
+template <int N>
+struct OddEvenNetHolder {
+    static constexpr OddEvenNet<N> net{};
+};
+
+// Comparators applied by template recursion, so every register index is a
+// compile-time constant however long the network is.
+template <int N, int C>
+struct OECmp {
+    static constexpr int n = OddEvenNetHolder<N>::net.n;
+    static constexpr int a = C < n ? OddEvenNetHolder<N>::net.a[C] : 0;
+    static constexpr int b = C < n ? OddEvenNetHolder<N>::net.b[C] : 0;
+};
+
+template <int N, int C, typename K>
+__device__ __forceinline__ void oddeven_apply(K (&v)[N]) {
+    if constexpr (C < OECmp<N, C>::n) {
+        cas(v[OECmp<N, C>::a], v[OECmp<N, C>::b]);
+        if constexpr (C + 1 < OECmp<N, C>::n) cas(v[OECmp<N, C + 1>::a], v[OECmp<N, C + 1>::b]);
+        if constexpr (C + 2 < OECmp<N, C>::n) cas(v[OECmp<N, C + 2>::a], v[OECmp<N, C + 2>::b]);
+        if constexpr (C + 3 < OECmp<N, C>::n) cas(v[OECmp<N, C + 3>::a], v[OECmp<N, C + 3>::b]);
+        oddeven_apply<N, C + 4>(v);
+    }
+}
+
 template <int N, typename K>
 __device__ __forceinline__ void oddeven_sort(K (&v)[N]) {
-    constexpr OddEvenNet<N> net{};
-#pragma unroll
-    for (int c = 0; c < net.n; ++c) cas(v[net.a[c]], v[net.b[c]]);
+    oddeven_apply<N, 0>(v);
 }
 
 

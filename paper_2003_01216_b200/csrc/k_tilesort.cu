@@ -12,7 +12,8 @@
 // SIMT lanes -- by the GPU shape of the same "sort the partitions, then merge
 // sorted lists pairwise" idea its parallel sorts are built from:
 //   1. each thread sorts VT keys in registers (Batcher odd-even network,
-//      compile-time register indices, no branches);
+//      compile-time register indices, no branches; VT = 53 int32 / 27 int64 --
+//      a longer network is cheaper than one more shared-memory round);
 //   2. log2(NT) merge-path merge rounds in shared memory turn the NT sorted
 //      runs into one (the binary-tree merge of P:58-60 at CTA scope).
 // Keys-only data makes the sorted tile unique, so the (unstable) network
@@ -23,22 +24,22 @@
 #include "hs_launch.h"
 
 #ifndef HS_SORT_NT
-#define HS_SORT_NT 512
+#define HS_SORT_NT 256
 #endif
 #ifndef HS_SORT_VT
-#define HS_SORT_VT 27
+#define HS_SORT_VT 53
 #endif
 #ifndef HS_SORT_MINB
-#define HS_SORT_MINB 2
+#define HS_SORT_MINB 4
 #endif
 #ifndef HS_SORT_NT64
-#define HS_SORT_NT64 512
+#define HS_SORT_NT64 256
 #endif
 #ifndef HS_SORT_VT64
-#define HS_SORT_VT64 15
+#define HS_SORT_VT64 27
 #endif
 #ifndef HS_SORT_MINB64
-#define HS_SORT_MINB64 2
+#define HS_SORT_MINB64 3
 #endif
 
 namespace hs {
