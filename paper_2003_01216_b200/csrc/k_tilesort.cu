@@ -24,22 +24,22 @@
 #include "hs_launch.h"
 
 #ifndef HS_SORT_NT
-#define HS_SORT_NT 256
+#define HS_SORT_NT 512
 #endif
 #ifndef HS_SORT_VT
 #define HS_SORT_VT 53
 #endif
 #ifndef HS_SORT_MINB
-#define HS_SORT_MINB 4
+#define HS_SORT_MINB 2
 #endif
 #ifndef HS_SORT_NT64
-#define HS_SORT_NT64 256
+#define HS_SORT_NT64 512
 #endif
 #ifndef HS_SORT_VT64
 #define HS_SORT_VT64 27
 #endif
 #ifndef HS_SORT_MINB64
-#define HS_SORT_MINB64 3
+#define HS_SORT_MINB64 2
 #endif
 
 namespace hs {
