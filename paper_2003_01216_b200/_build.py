@@ -15,6 +15,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libhybridsort.so")
+SO_DEBUG = os.path.join(HERE, "libhybridsort_debug.so")  # -DHS_DEBUG: device invariant checks
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -42,22 +43,29 @@ def _inputs() -> list[str]:
 
 
 def needs_build() -> bool:
-    if not os.path.exists(SO):
+    return needs_build_at(SO)
+
+
+def needs_build_at(so: str) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     return any(os.path.getmtime(p) > t for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return SO
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", SO + ".tmp", *sources()]
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """Build libhybridsort.so (or, debug=True, libhybridsort_debug.so with -DHS_DEBUG)."""
+    so = SO_DEBUG if debug else SO
+    if not force and not needs_build_at(so):
+        return so
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DHS_DEBUG"] if debug else []), "-I", INCLUDE, "-I", CSRC, "-o", so + ".tmp",
+           *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":

@@ -9,6 +9,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side invariant checks of the debug build (libhybridsort_debug.so,
+// -DHS_DEBUG; tests/test_debug_build.py): shared-memory indices, piece
+// geometry, scatter positions.  compute-sanitizer is closed on this pool, so
+// these asserts stand in for it.  Compiled out of the product library.
+#ifdef HS_DEBUG
+#include <cstdio>
+#define HS_DASSERT(c)                                                                          \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("HS_DASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                         \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define HS_DASSERT(c) \
+    do {              \
+    } while (0)
+#endif
+
 namespace hs {
 
 // --------------------------------------------------------------- key traits

@@ -130,6 +130,7 @@ __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, c
             else r = mid;
         }
     }
+    HS_DASSERT(l >= 0 && l <= na && diag - l >= 0 && diag - l <= nb);
     corank[beta] = (int)(g.a_lo + l);
 }
 
@@ -284,6 +285,10 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
         mbar_wait(&full[slot], (it / ST) & 1);
         const Piece<K> q = pc[slot];
         if (q.len < 0) break;
+        HS_DASSERT(q.na >= 0 && q.nb >= 0 && q.na + q.nb == q.len && q.len <= TM);
+        // (an empty A slice has no bytes in the stage; its offA is only the phase)
+        HS_DASSERT(q.offA >= 0 && q.offA + q.na <= SLOT && (q.na == 0 || q.offB >= q.offA + q.na) &&
+                   q.offB >= 0 && q.offB + q.nb <= SLOT);
         const K *sb = stage0 + slot * SLOT;
         const K *A = sb + q.offA;
         const K *B = sb + q.offB;
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
                 if (k + 1 < VT) {
                     const int nx = (p ? ai : bi) + 1;
                     const int lim = p ? a_end : b_end;
+                    HS_DASSERT(nx >= 0 && nx < SLOT);
                     const K t = sb[nx];
                     const K tv = nx < lim ? t : kMax;
                     ai = p ? nx : ai;

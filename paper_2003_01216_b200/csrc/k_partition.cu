@@ -270,6 +270,7 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
     constexpr int E = 16 / sizeof(K);
     constexpr int NW = NT / 32;
     constexpr int NMETA = VT / 4 > 0 ? VT / 4 : 1;
+    [[maybe_unused]] constexpr int T_ = NT * VT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     unsigned meta[NMETA];
@@ -371,6 +372,7 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
             if (FULL || d < 10) {
                 const unsigned wsel = d < 2 ? base[0] : d < 4 ? base[1] : d < 6 ? base[2] : d < 8 ? base[3] : base[4];
                 const int pos = (int)((wsel >> ((d & 1u) * 16)) & 0xFFFFu) + (int)r;
+                HS_DASSERT(pos >= 0 && pos < T_ && d < 10);
                 sOut[pos] = kv[e];
                 sDig[pos] = (uint8_t)d;
             }
@@ -380,7 +382,10 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
 
     // ten coalesced runs
     const int nvalid = jhi - jlo;
-    for (int j = tid; j < nvalid; j += NT) out[s_delta[sDig[j]] + j] = sOut[j];
+    for (int j = tid; j < nvalid; j += NT) {
+        HS_DASSERT(sDig[j] < 10);
+        out[s_delta[sDig[j]] + j] = sOut[j];
+    }
 }
 
 // Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the next

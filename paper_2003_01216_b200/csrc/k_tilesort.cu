@@ -102,19 +102,6 @@ __device__ __forceinline__ void bulk_s2g_ts(void *dst, const void *src, uint32_t
                  : "memory");
 }
 
-// Merge-path split of output diag between A = sm[a0, a0+na) and B = sm[b0, b0+nb) (stable-left).
-template <typename K>
-__device__ __forceinline__ int smem_merge_path(const K *sm, int a0, int na, int b0, int nb, int diag) {
-    int l = diag - nb > 0 ? diag - nb : 0;
-    int r = diag < na ? diag : na;
-    while (l < r) {
-        const int mid = (l + r) >> 1;
-        if (sm[a0 + mid] <= sm[b0 + diag - 1 - mid]) l = mid + 1;
-        else r = mid;
-    }
-    return l;
-}
-
 template <typename K>
 __device__ __forceinline__ K lds_k(uint32_t a);
 template <>
@@ -162,6 +149,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     const long long lo = leaf_start(P, b, i);
     const int len = (int)(leaf_start(P, b, i + 1) - lo);
     if (len == 0) return;
+    HS_DASSERT(len > 0 && len <= T && lo >= P.off[b] && lo + len <= P.off[b + 1]);
     K *const out = ((P.L[b] & 1) ? S : F) + lo;  // where this bucket's merge level 0 reads
     const K kMax = KeyTraits<K>::kMax;
 
@@ -227,6 +215,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
             }
             uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
             uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
+            HS_DASSERT(l >= 0 && l <= RL && diag - l >= 0 && diag - l <= RL && bE <= T);
+            [[maybe_unused]] const uint32_t lo_b = ua, hi_b = sm_u + (uint32_t)bE * sizeof(K);  // the pair's stretch
             K x = lds_k<K>(pi), y = lds_k<K>(pj);
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
@@ -235,6 +225,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 if (k + 1 < VT) {
                     pi += p ? (uint32_t)sizeof(K) : 0u;
                     pj -= p ? 0u : (uint32_t)sizeof(K);
+                    HS_DASSERT(pi >= lo_b && pi < hi_b && pj >= lo_b && pj < hi_b);
                     const K t = lds_k<K>(p ? pi : pj);
                     x = p ? t : x;
                     y = p ? y : t;
