@@ -17,7 +17,7 @@ from paper_2003_01216_b200 import _build
 
 
 def main():
-    lib = ctypes.CDLL(_build.SO_DEBUG)
+    lib = ctypes.CDLL(os.environ.get("HS_DEBUG_LIB", _build.SO_DEBUG))
     vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
     lib.hs_msd_partition.argtypes = [vp, i64, ci, ci, vp, vp, vp]
