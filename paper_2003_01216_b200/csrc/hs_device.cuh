@@ -323,13 +323,32 @@ struct OECmp {
 };
 
 template <int N, int C, typename K>
+__device__ __forceinline__ void oddeven_cmp(K (&v)[N]) {
+    if constexpr (C < OECmp<N, C>::n) cas(v[OECmp<N, C>::a], v[OECmp<N, C>::b]);
+}
+
+// 16 comparators per recursion level (keeps the instantiation depth low for
+// long networks)
+template <int N, int C, typename K>
 __device__ __forceinline__ void oddeven_apply(K (&v)[N]) {
     if constexpr (C < OECmp<N, C>::n) {
-        cas(v[OECmp<N, C>::a], v[OECmp<N, C>::b]);
-        if constexpr (C + 1 < OECmp<N, C>::n) cas(v[OECmp<N, C + 1>::a], v[OECmp<N, C + 1>::b]);
-        if constexpr (C + 2 < OECmp<N, C>::n) cas(v[OECmp<N, C + 2>::a], v[OECmp<N, C + 2>::b]);
-        if constexpr (C + 3 < OECmp<N, C>::n) cas(v[OECmp<N, C + 3>::a], v[OECmp<N, C + 3>::b]);
-        oddeven_apply<N, C + 4>(v);
+        oddeven_cmp<N, C + 0>(v);
+        oddeven_cmp<N, C + 1>(v);
+        oddeven_cmp<N, C + 2>(v);
+        oddeven_cmp<N, C + 3>(v);
+        oddeven_cmp<N, C + 4>(v);
+        oddeven_cmp<N, C + 5>(v);
+        oddeven_cmp<N, C + 6>(v);
+        oddeven_cmp<N, C + 7>(v);
+        oddeven_cmp<N, C + 8>(v);
+        oddeven_cmp<N, C + 9>(v);
+        oddeven_cmp<N, C + 10>(v);
+        oddeven_cmp<N, C + 11>(v);
+        oddeven_cmp<N, C + 12>(v);
+        oddeven_cmp<N, C + 13>(v);
+        oddeven_cmp<N, C + 14>(v);
+        oddeven_cmp<N, C + 15>(v);
+        oddeven_apply<N, C + 16>(v);
     }
 }
 
