@@ -424,7 +424,10 @@ def run_dist(args, cfg):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        out, info = hd.dist_sort(buf, cfg.num_digits, cfg.chunks)
+        if args.fused:
+            out, info = hd.dist_sort_fused(buf, cfg.num_digits, cfg.chunks)
+        else:
+            out, info = hd.dist_sort(buf, cfg.num_digits, cfg.chunks)
         b.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
@@ -439,7 +442,9 @@ def run_dist(args, cfg):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
                 "config": {"workload": workload_desc(cfg) + f" per rank (keys [rank*n, (rank+1)*n) of the stream)",
-                           "parallelism": f"bucket sharding over NCCL: {world} ranks (SURVEY f2, P:78-80)",
+                           "parallelism": (f"bucket sharding, exchange fused into the scatter (peer stores into "
+                                           f"symmetric memory): {world} ranks (SURVEY f2, P:78-80)" if args.fused else
+                                           f"bucket sharding over NCCL all-to-all-v: {world} ranks (SURVEY f2, P:78-80)"),
                            "group_start": info.group_start, "max_group_keys": info.max_load,
                            "timing": "CUDA events around dist_sort (partition, size all-gather, all-to-all-v, "
                                      "local hs_sort), max over ranks"},
@@ -461,6 +466,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
+    ap.add_argument("--fused", action="store_true", help="with --dist: exchange fused into the scatter kernel")
     args = ap.parse_args()
     import workload as W
     cfg = W.CONFIGS[args.config]

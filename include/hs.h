@@ -184,6 +184,28 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
                           cudaStream_t stream);
 
 /*
+ * SURVEY §8(f) row f2, the sender side of the paper's cluster model with the
+ * bucket exchange fused into the scatter (§3.4, "divides the data
+ * into ten parts ... Then sends each bucket or buckets to proper node").
+ * hs_partition_plan_create runs a1-a2 (tile histograms + lookback prefix) of
+ * keys and writes the local bucket_offsets[11] (device); the caller learns
+ * the sizes, agrees on an exchange layout with its peers, and then
+ * hs_partition_scatter runs a3 writing the key at local bucket position p of
+ * digit d straight to dst[d] + (p - bucket_offsets[d]).  dst[d] (host array of
+ * 10 device pointers; NULL for an empty bucket) may point into a PEER GPU's
+ * memory (CUDA IPC / symmetric memory over NVLink), so the exchange costs no
+ * staging copy and no collective call.  Stability as hs_msd_partition.
+ *   keys[n] must stay unchanged between create and scatter; the plan owns
+ *   stream-ordered scratch released by hs_partition_plan_destroy (same stream).
+ *   Errors as hs_msd_partition; dst entries must be dtype-aligned.
+ */
+typedef struct hs_partition_plan_s *hs_partition_plan_t;
+hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits,
+                                     int64_t *bucket_offsets, hs_partition_plan_t *plan, cudaStream_t stream);
+hs_status_t hs_partition_scatter(hs_partition_plan_t plan, void *const *dst, cudaStream_t stream);
+hs_status_t hs_partition_plan_destroy(hs_partition_plan_t plan, cudaStream_t stream);
+
+/*
  * SURVEY §8(f) row f2, host side of the paper's cluster model (§3.4 Fig 4,
  * P:80 "sends each bucket or buckets to proper node"
  * assign_buckets): split the ten digits into `nodes` contiguous groups of at

@@ -22,7 +22,7 @@ __all__ = [
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
-    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline",
+    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan",
 ]
 
 HS_INT32, HS_INT64 = 0, 1
@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
     "hs_msd_partition_pairs", "hs_sort_pairs",
+    "hs_partition_plan_create", "hs_partition_scatter", "hs_partition_plan_destroy",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy")
 
@@ -88,6 +89,12 @@ def load(path: str | None = None):
     lib.hs_plan_levels.restype = ci
     lib.hs_assign_buckets.argtypes = [vp, ci, vp, vp]
     lib.hs_assign_buckets.restype = ci
+    lib.hs_partition_plan_create.argtypes = [vp, i64, ci, ci, vp, ctypes.POINTER(vp), vp]
+    lib.hs_partition_plan_create.restype = ci
+    lib.hs_partition_scatter.argtypes = [vp, ctypes.POINTER(vp), vp]
+    lib.hs_partition_scatter.restype = ci
+    lib.hs_partition_plan_destroy.argtypes = [vp, vp]
+    lib.hs_partition_plan_destroy.restype = ci
     if path is None:
         _LIB = lib
     return lib
@@ -301,6 +308,43 @@ def hs_sort_pairs(keys, tags, num_digits: int, chunks_per_bucket: int = 8, strea
         _check(load().hs_sort_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, chunks_per_bucket,
                                     _stream(stream)))
     return keys, tags
+
+
+class PartitionPlan:
+    """a1-a2 now, a3 later into caller-chosen (possibly peer-GPU) destinations:
+    hs_partition_plan_create / hs_partition_scatter / hs_partition_plan_destroy
+    (the bucket exchange fused into the scatter)."""
+
+    def __init__(self, keys, num_digits: int, stream=None):
+        torch = _torch()
+        _check_tensor(keys, "keys")
+        self.keys = keys  # must stay alive and unchanged until scatter()
+        self.dt = _dtype_code(keys)
+        self.stream = stream
+        self.offsets = torch.empty(11, dtype=torch.int64, device=keys.device)
+        self.handle = ctypes.c_void_p()
+        with torch.cuda.device(keys.device):
+            _check(load().hs_partition_plan_create(keys.data_ptr(), keys.numel(), self.dt, num_digits,
+                                                   self.offsets.data_ptr(), ctypes.byref(self.handle),
+                                                   _stream(stream)))
+
+    def scatter(self, dst_ptrs) -> None:
+        """dst_ptrs: 10 device addresses (ints; 0 for empty buckets)."""
+        torch = _torch()
+        arr = (ctypes.c_void_p * 10)(*[int(p) if p else None for p in dst_ptrs])
+        with torch.cuda.device(self.keys.device):
+            _check(load().hs_partition_scatter(self.handle, arr, _stream(self.stream)))
+
+    def close(self) -> None:
+        if self.handle:
+            load().hs_partition_plan_destroy(self.handle, _stream(self.stream))
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=None, out=None):

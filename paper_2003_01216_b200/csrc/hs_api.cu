@@ -480,6 +480,81 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     return HS_OK;
 }
 
+struct hs_partition_plan_s {
+    const void *keys;
+    int64_t n;
+    hs_dtype_t dtype;
+    int h;
+    unsigned long long div, magic;
+    int sms;
+    Workspace ws;
+};
+
+hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits,
+                                     int64_t *bucket_offsets, hs_partition_plan_t *plan, cudaStream_t stream) {
+    hs_status_t s;
+    if (!plan) return fail(HS_ERR_INVALID_VALUE, "plan is NULL");
+    *plan = nullptr;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if (!bucket_offsets || ((uintptr_t)bucket_offsets & 7) != 0)
+        return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL or not 8-byte aligned");
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    hs_partition_plan_s *p = new hs_partition_plan_s();
+    p->keys = keys;
+    p->n = n;
+    p->dtype = dtype;
+    p->sms = sms;
+    const int dt = (int)dtype;
+    const int Tp = hs::scatter_tile_keys(dt);
+    p->h = (int)(((uintptr_t)keys % 16) / ksize(dtype));
+    const long long tiles = (n + p->h + Tp - 1) / Tp;
+    digit_params(num_digits, dtype, &p->div, &p->magic);
+    if ((s = ws_alloc(&p->ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, 0, stream)) != HS_OK) {
+        delete p;
+        return s;
+    }
+    Workspace &ws = p->ws;
+    if ((e = cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream)) != cudaSuccess ||
+        (e = hs::launch_partition(dt, keys, nullptr, (int)n, p->h, p->div, p->magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                  ws.status, (long long *)bucket_offsets, -1, 0, 0, sms, false, stream)) != cudaSuccess) {
+        cudaFreeAsync(ws.base, stream);
+        delete p;
+        return cuda_fail(e, "K1-K2 count");
+    }
+    *plan = p;
+    g_launches = tiles > 0 ? 2 : 1;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_partition_scatter(hs_partition_plan_t plan, void *const *dst, cudaStream_t stream) {
+    if (!plan || !dst) return fail(HS_ERR_INVALID_VALUE, "plan or dst is NULL");
+    const int ks = ksize(plan->dtype);
+    for (int d = 0; d < 10; ++d)
+        if (dst[d] && ((uintptr_t)dst[d] % ks) != 0)
+            return fail(HS_ERR_INVALID_VALUE, "dst[%d] is not %d-byte aligned", d, ks);
+    Workspace &ws = plan->ws;
+    cudaError_t e = hs::launch_partition((int)plan->dtype, plan->keys, nullptr, (int)plan->n, plan->h, plan->div,
+                                         plan->magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status, nullptr, -1, 0, 0,
+                                         plan->sms, true, stream, 0, false, dst);
+    if (e != cudaSuccess) return cuda_fail(e, "K3 scatter");
+    g_launches = plan->n > 0 ? 1 : 0;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_partition_plan_destroy(hs_partition_plan_t plan, cudaStream_t stream) {
+    if (!plan) return HS_OK;
+    cudaError_t e = cudaFreeAsync(plan->ws.base, stream);
+    delete plan;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    return HS_OK;
+}
+
 hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, int64_t n, int num_digits,
                                    int64_t *bucket_offsets, int32_t *out_keys, uint64_t *out_tags,
                                    cudaStream_t stream) {

@@ -28,7 +28,7 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
                              unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
                              int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st,
-                             int key_shift = 0);
+                             int key_shift = 0, bool do_count = true, void *const *dst10 = nullptr);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,

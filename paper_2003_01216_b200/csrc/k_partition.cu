@@ -254,6 +254,17 @@ __global__ void __launch_bounds__(kScanNT) k_tile_scan(const uint32_t *__restric
 }
 
 // =================================================================== K3
+// Where digit d's keys go: out (one array, CSR by bucket) unless `use`, in
+// which case the key at local bucket position p of digit d is stored to
+// dst[d] + (p - off[d]) -- dst[d] may be a peer GPU's buffer (NVLink P2P /
+// symmetric memory): the cluster model's bucket exchange fused into the
+// scatter (hs_partition_scatter).
+template <typename K>
+struct DstTable {
+    K *dst[10];
+    int use;
+};
+
 template <typename K, int NT, int VT>
 struct ScatSmem {
     static constexpr int T = NT * VT;
@@ -266,7 +277,8 @@ template <typename K, int NT, int VT, bool FULL>
 __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__restrict__ sOut, uint8_t *sDig,
                                              K *__restrict__ out, int jlo, int jhi, int tile, const DigitParams<K> &dp,
                                              const Ctl *__restrict__ ctl, const uint32_t *__restrict__ tile_pref,
-                                             unsigned (*s_wtot)[5], int *s_dstart, int *s_delta) {
+                                             unsigned (*s_wtot)[5], int *s_dstart, K **s_dptr,
+                                             const DstTable<K> &dtab) {
     constexpr int E = 16 / sizeof(K);
     constexpr int NW = NT / 32;
     constexpr int NMETA = VT / 4 > 0 ? VT / 4 : 1;
@@ -349,7 +361,8 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
             }
             s_dstart[lane] = (int)dstart;
             // global position of tile-local slot j of digit d = delta[d] + j (< 2^31)
-            s_delta[lane] = (int)(ctl->off[lane] + (long long)tile_pref[(size_t)tile * 10 + lane] - (long long)dstart);
+            const long long delta = ctl->off[lane] + (long long)tile_pref[(size_t)tile * 10 + lane] - (long long)dstart;
+            s_dptr[lane] = (dtab.use ? dtab.dst[lane] - ctl->off[lane] : out) + delta;
         }
     }
     __syncthreads();
@@ -384,7 +397,7 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
     const int nvalid = jhi - jlo;
     for (int j = tid; j < nvalid; j += NT) {
         HS_DASSERT(sDig[j] < 10);
-        out[s_delta[sDig[j]] + j] = sOut[j];
+        s_dptr[sDig[j]][j] = sOut[j];
     }
 }
 
@@ -394,7 +407,7 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
 template <typename K, int NT, int VT>
 __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *__restrict__ out, int n, int h,
                                                 DigitParams<K> dp, const Ctl *__restrict__ ctl,
-                                                const uint32_t *__restrict__ tile_pref, int ntiles) {
+                                                const uint32_t *__restrict__ tile_pref, int ntiles, DstTable<K> dtab) {
     constexpr int T = NT * VT;
     constexpr int NW = NT / 32;
     static_assert(VT <= 16 && T <= 16384, "packing limits");
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ unsigned s_wtot[NW][5];
     __shared__ int s_dstart[10];
-    __shared__ int s_delta[10];
+    __shared__ K *s_dptr[10];
     const int tid = threadIdx.x;
 
     // virtual tile t covers [t*T - h, (t+1)*T - h): 16-byte aligned in memory
@@ -437,10 +450,10 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
         const K *stage = stage0 + slot * T;
         if (jlo == 0 && jhi == T)
             scatter_tile<K, NT, VT, true>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
-                                          s_delta);
+                                          s_dptr, dtab);
         else
             scatter_tile<K, NT, VT, false>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
-                                           s_delta);
+                                           s_dptr, dtab);
         __syncthreads();  // stage / sOut / tables are reused next iteration
     }
 }
@@ -455,7 +468,8 @@ template <typename K>
 cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsigned long long div,
                                unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                                unsigned long long *status, long long *user_off, int plan_mode, int log2c,
-                               int sort_tile_keys, int num_sms, bool do_scatter, int key_shift, cudaStream_t st) {
+                               int sort_tile_keys, int num_sms, bool do_scatter, int key_shift, cudaStream_t st,
+                               bool do_count, void *const *dst10) {
     using G = PGeo<K>;
     constexpr int TP = G::kScatNT * G::kScatVT;
     DigitParams<K> dp;
@@ -463,7 +477,7 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     dp.magic = (typename KeyTraits<K>::U)magic;
     dp.shift = key_shift;
     const long long ntiles = ((long long)n + h + TP - 1) / TP;
-    if (ntiles > 0) {
+    if (do_count && ntiles > 0) {
         long long want = (ntiles + kHistWarps - 1) / kHistWarps;
         int grid = (int)(want > 8LL * num_sms ? 8LL * num_sms : want);
         prof_begin(kProfTileHist, st);
@@ -474,11 +488,14 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     }
     const long long per = (long long)kScanNT * kScanIPT;
     const int sgrid = (int)(ntiles > 0 ? (ntiles + per - 1) / per : 1);
-    prof_begin(kProfTileScan, st);
-    k_tile_scan<<<sgrid, kScanNT, 0, st>>>(tile_hist, tile_pref, (int)ntiles, status, ctl, user_off, plan_mode, log2c,
-                                           sort_tile_keys);
-    prof_end(kProfTileScan, st);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    if (do_count) {
+        prof_begin(kProfTileScan, st);
+        k_tile_scan<<<sgrid, kScanNT, 0, st>>>(tile_hist, tile_pref, (int)ntiles, status, ctl, user_off, plan_mode,
+                                               log2c, sort_tile_keys);
+        prof_end(kProfTileScan, st);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
     auto kern = k_scatter<K, G::kScatNT, G::kScatVT>;
@@ -498,8 +515,11 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     long long grid = (long long)per_sm * num_sms;
     if (grid > ntiles) grid = ntiles;
     prof_begin(kProfScatter, st);
+    DstTable<K> dtab;
+    dtab.use = dst10 != nullptr;
+    for (int d = 0; d < 10; ++d) dtab.dst[d] = dst10 ? (K *)dst10[d] : nullptr;
     kern<<<(unsigned)grid, G::kScatNT, SS::bytes(), st>>>((const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
-                                                          (int)ntiles);
+                                                          (int)ntiles, dtab);
     prof_end(kProfScatter, st);
     return cudaGetLastError();
 }
@@ -514,12 +534,14 @@ int scan_ctas(long long ntiles) {
 cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, unsigned long long div,
                              unsigned long long magic, Ctl *ctl, uint32_t *tile_hist, uint32_t *tile_pref,
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
-                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st, int key_shift) {
+                             int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st, int key_shift,
+                             bool do_count, void *const *dst10) {
     return dt == 0 ? launch_partition_t<int32_t>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status,
-                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, 0, st)
+                                                 user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, 0, st,
+                                                 do_count, dst10)
                    : launch_partition_t<int64_t>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status,
                                                  user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter,
-                                                 key_shift, st);
+                                                 key_shift, st, do_count, dst10);
 }
 
 }  // namespace hs

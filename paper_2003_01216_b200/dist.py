@@ -29,8 +29,15 @@ The global result is the concatenation of the ranks' outputs in rank order
 (``gather_to`` assembles it on one rank, the paper's final gather).  With
 more than 10 ranks the extra ranks own no digit (at most ten nodes).
 
-The exchange runs through the collectives of the process group, NCCL on
-GPUs.  The per-rank steps 1 and 5 are injected as ``ops`` so the host logic
+``dist_sort`` runs the exchange through the collectives of the process group
+(NCCL on GPUs).  ``dist_sort_fused`` fuses it into the scatter instead: each
+rank's K3 stores every digit's keys straight into the owner rank's
+symmetric-memory receive buffer over NVLink (hs_partition_scatter with peer
+destination pointers), so step 4 costs no collective call and no staging copy,
+and the owner's buffer arrives already partitioned by digit (steps 5 is then
+chunk sort + tree merge, no second MSD pass).
+
+In ``dist_sort`` the per-rank steps 1 and 5 are injected as ``ops`` so the host logic
 can be tested on CPU with the gloo backend (tests/test_dist.py passes
 oracle-based ops there); the default ops are the CUDA path and there is no
 CPU fallback in it.
@@ -39,7 +46,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import assign_buckets, hs_msd_partition, hs_sort
+from . import PartitionPlan, assign_buckets, hs_merge, hs_msd_partition, hs_sort, hs_sort_chunks
 
 
 @dataclass
@@ -113,3 +120,105 @@ def gather_to(local_sorted, dst: int = 0, group=None):
     out = torch.empty(sum(recv), dtype=local_sorted.dtype, device=local_sorted.device)
     dist.all_to_all_single(out, local_sorted, output_split_sizes=recv, input_split_sizes=send, group=group)
     return out if rank == dst else None
+
+
+# ----------------------------------------------------------------- fused exchange
+def exchange_layout(sizes, group_start):
+    """Where every (source rank, digit) segment lands in its owner's receive buffer.
+
+    sizes[r][d]: keys of digit d on rank r.  Owner g's buffer holds its digits
+    in ascending order, each digit's segments in source-rank order -- i.e. it
+    is already partitioned by digit, ready for the per-bucket chunk sort and
+    tree merge.  Returns (owner[d], offset[r][d], recv_offsets[g] (11 entries),
+    recv_total[g]).  Pure host logic (tests/test_dist.py checks it on CPU).
+    """
+    world = len(sizes)
+    total = [sum(sizes[r][d] for r in range(world)) for d in range(10)]
+    owner = [0] * 10
+    for g in range(len(group_start) - 1):
+        for d in range(group_start[g], group_start[g + 1]):
+            owner[d] = g
+    offset = [[0] * 10 for _ in range(world)]
+    recv_offsets, recv_total = [], []
+    for g in range(world):
+        off = [0] * 11
+        pos = 0
+        for d in range(10):
+            if g < len(group_start) - 1 and owner[d] == g:
+                for r in range(world):
+                    offset[r][d] = pos + sum(sizes[rr][d] for rr in range(r))
+                pos += total[d]
+            off[d + 1] = pos
+        recv_offsets.append(off)
+        recv_total.append(pos)
+    return owner, offset, recv_offsets, recv_total
+
+
+class _SymmBuffer:
+    """Cached symmetric-memory receive buffer (re-made only when it must grow)."""
+
+    def __init__(self):
+        self.buf = self.handle = None
+        self.key = None
+
+    def get(self, numel, dtype, device, group):
+        import torch.distributed._symmetric_memory as symm_mem
+        if self.buf is None or self.buf.numel() < numel or self.key != (dtype, device):
+            cap = max(numel, 1)
+            import torch.distributed as dist
+            self.buf = symm_mem.empty(cap, dtype=dtype, device=device)
+            self.handle = symm_mem.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+            self.key = (dtype, device)
+        return self.buf, self.handle
+
+
+_SYMM = _SymmBuffer()
+
+
+def dist_sort_fused(keys, num_digits: int, chunks: int = 8, group=None):
+    """dist_sort with the bucket exchange fused into the scatter kernel.
+
+    Every rank's K3 writes each digit's keys straight into the owner rank's
+    symmetric-memory receive buffer over NVLink (peer stores from the kernel,
+    hs_partition_scatter) -- no all-to-all call and no staging copy; then every
+    owner chunk-sorts and tree-merges its received buckets in place.  Returns
+    (local_sorted view, DistInfo).  CUDA + NCCL process group only.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    plan = PartitionPlan(keys, num_digits)
+    off = plan.offsets
+    local_sizes = (off[1:] - off[:-1]).contiguous()
+    gathered = [torch.empty_like(local_sizes) for _ in range(world)]
+    dist.all_gather(gathered, local_sizes, group=group)
+    sizes = torch.stack(gathered).cpu().tolist()
+    global_sizes = [sum(sizes[r][d] for r in range(world)) for d in range(10)]
+    nodes = min(world, 10)
+    group_start, max_load = assign_buckets(global_sizes, nodes)
+    owner, offset, recv_offsets, recv_total = exchange_layout(sizes, group_start)
+    buf, handle = _SYMM.get(max(recv_total), keys.dtype, keys.device, group)
+    handle.barrier()  # every owner's buffer is free (previous call finished reading it)
+    esz = keys.element_size()
+    dst = []
+    for d in range(10):
+        if sizes[rank][d] == 0:
+            dst.append(0)
+            continue
+        peer = handle.get_buffer(owner[d], (buf.numel(),), keys.dtype)
+        dst.append(peer.data_ptr() + offset[rank][d] * esz)
+    plan.scatter(dst)
+    torch.cuda.current_stream().synchronize()
+    plan.close()
+    handle.barrier()  # every rank's stores into this rank's buffer have landed
+    n_local = recv_total[rank] if rank < len(recv_total) else 0
+    local = buf[:n_local]
+    if n_local:
+        roff = torch.tensor(recv_offsets[rank], dtype=torch.int64, device=keys.device)
+        hs_sort_chunks(local, roff, chunks, out=local)
+        hs_merge(local, roff, chunks, out=local)
+    send = [sum(sizes[rank][d] for d in range(10) if owner[d] == g) for g in range(world)]
+    recv = [sum(sizes[r][d] for d in range(10) if owner[d] == rank) for r in range(world)]
+    return local, DistInfo(group_start, global_sizes, send, recv, max_load)

@@ -172,3 +172,60 @@ def test_dist_sort_one_rank_nccl():
         assert info.group_start == [0, 10] and info.send_counts == [keys.size]
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ fused exchange layout (CPU)
+def test_exchange_layout_simulated():
+    """The fused exchange's layout: every (rank, digit) segment lands once, owners' buffers are
+    partitioned by digit, and chunk sort + tree merge of each buffer gives the sorted union."""
+    from paper_2003_01216_b200.dist import exchange_layout
+    import paper_2003_01216_b200 as hs
+    rng = np.random.default_rng(80)
+    for world in (1, 2, 3, 4, 12):
+        keys = [W.uniform(int(rng.integers(0, 3000)), 10 + r, 10**6, dtype=np.int32) for r in range(world)]
+        if world > 1:
+            keys[1][: keys[1].size // 2] = 400_000 + keys[1][: keys[1].size // 2] % 1000  # skew
+        parts = [O.msd_partition(k, 6) for k in keys]
+        sizes = [np.diff(off).tolist() for _, off in parts]
+        gs, _ = hs.assign_buckets([sum(s[d] for s in sizes) for d in range(10)], min(world, 10))
+        owner, offset, roff, rtot = exchange_layout(sizes, gs)
+        bufs = [np.full(t, -1, dtype=np.int32) for t in rtot]
+        for r, (part, off) in enumerate(parts):       # what every rank's fused scatter stores
+            for d in range(10):
+                seg = part[off[d]:off[d + 1]]
+                b = bufs[owner[d]]
+                assert (b[offset[r][d]:offset[r][d] + seg.size] == -1).all()   # written once
+                b[offset[r][d]:offset[r][d] + seg.size] = seg
+        out = []
+        for g in range(world):
+            assert (bufs[g] >= 0).all()                                         # fully covered
+            if bufs[g].size:
+                d = O.histogram(bufs[g], 6)
+                assert np.array_equal(np.diff(roff[g]), d)                      # partitioned by digit
+                x = O.sort_chunks(bufs[g], np.array(roff[g]), 8)
+                out.append(O.merge(x, np.array(roff[g]), 8))
+        allk = np.concatenate(keys)
+        assert np.array_equal(np.concatenate(out) if out else allk[:0], np.sort(allk))
+
+
+@pytest.mark.gpu
+def test_dist_sort_fused_one_rank():
+    """The fused path end to end on one rank: K1-K2, symmetric-memory buffer, K3 storing into it
+    through peer pointers (self), chunk sort + tree merge in place."""
+    import torch.distributed as dist
+    from paper_2003_01216_b200 import dist as hd
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for name, n in (("C1", None), ("C4", 2_000_000), ("P3", 1_000_000)):
+            cfg = W.CONFIGS[name]
+            keys = W.generate(name, 0, n)
+            local, info = hd.dist_sort_fused(torch.from_numpy(keys).cuda(), cfg.num_digits, 8)
+            torch.cuda.synchronize()
+            assert np.array_equal(local.cpu().numpy(), O.sort(keys, cfg.num_digits, 8)), name
+            assert info.send_counts == [keys.size]
+    finally:
+        dist.destroy_process_group()
