@@ -389,3 +389,29 @@ def test_host_sort_pipeline():
     pipe.finish()
     for i, b in enumerate(h_out):
         assert_same(b.numpy(), O.sort(batches[i], 9, 8), f"pipeline batch {i}")
+
+
+@pytest.mark.slow
+def test_max_size_int32():
+    """n = 2^31 - 1 (the API's largest n; 8 GiB of keys + 8 GiB scratch): every position
+    computation of the path at its limit.  Checked with torch on the device (not our kernels):
+    nondecreasing, multiset sums of k and k^2 equal to the input's, bucket offsets equal to a bincount of
+    leading digits; plus one whole bucket compared with np.sort."""
+    n = 2**31 - 1
+    keys = W.uniform(n, 2031, 10**9, dtype=np.int32)
+    d = torch.from_numpy(keys).to(DEV)
+    d64 = d.to(torch.int64)
+    fp_in = (int(d64.sum()), int((d64 * d64).sum()))  # multiset invariants (wrapping int64)
+    del d64
+    counts = torch.bincount(torch.clamp(d // 10**8, 0, 9).to(torch.int64), minlength=10).cpu().numpy()
+    hs.hs_sort(d, 9, 8)
+    torch.cuda.synchronize()
+    assert bool(torch.all(d[1:] >= d[:-1]))
+    d64 = d.to(torch.int64)
+    fp_out = (int(d64.sum()), int((d64 * d64).sum()))
+    del d64
+    assert fp_in == fp_out
+    off = np.concatenate([[0], np.cumsum(counts)])
+    lo, hi = int(off[5]), int(off[6])
+    bucket = keys[(keys // 10**8) == 5]
+    assert_same(d[lo:hi].cpu().numpy(), np.sort(bucket), "bucket 5 at n = 2^31 - 1")
