@@ -200,8 +200,16 @@ def run_ours(args, cfg):
         tags0 = torch.arange(cfg.n, dtype=torch.int64, device=dev)
         tags = torch.empty_like(tags0)
 
+    graph = None
+    if args.graph:
+        if shared or pairs:
+            raise SystemExit("--graph applies to hs_sort")
+        graph = hs.SortGraph(buf, cfg.num_digits, cfg.chunks)
+
     def sort_step():
-        if shared:
+        if graph is not None:
+            graph.replay()
+        elif shared:
             hs.hs_sort_shared(buf, cfg.chunks)
         elif pairs:
             hs.hs_sort_pairs(buf, tags, cfg.num_digits, cfg.chunks)
@@ -221,6 +229,9 @@ def run_ours(args, cfg):
     ok = bool(torch.all(buf[1:] >= buf[:-1]).item())
     if not ok:
         raise SystemExit("[bench] hs_sort output is not sorted")
+    if graph is not None:
+        hs.hs_sort(buf, cfg.num_digits, cfg.chunks)  # launch count of one call (the graph replays them)
+        torch.cuda.synchronize()
     launches_per_step = hs.last_launch_count()
 
     def barrier():
@@ -254,7 +265,10 @@ def run_ours(args, cfg):
     hs.profile_enable(True)
     for _ in range(args.steps):
         restore()
-        sort_step()
+        if graph is not None:  # per-kernel events need the direct call (a replay records none)
+            hs.hs_sort(buf, cfg.num_digits, cfg.chunks)
+        else:
+            sort_step()
     prof = hs.profile_read()
     hs.profile_enable(False)
     # algorithmic bytes of the dominant kernel from the plan of this workload
@@ -361,7 +375,8 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n_per_gpu": cfg.n, "num_digits": cfg.num_digits,
                        "api": ("hs_sort_shared (no MSD step, SURVEY f1)" if shared else
-                               "hs_sort_pairs (int32 key + 64-bit tag items, stable; SURVEY f3)" if pairs else "hs_sort"),
+                               "hs_sort_pairs (int32 key + 64-bit tag items, stable; SURVEY f3)" if pairs else
+                               "hs_sort replayed from a CUDA graph (SortGraph)" if graph is not None else "hs_sort"),
                        "chunks_per_bucket": cfg.chunks, "merge_levels": max(levels),
                        "parallelism": "replicas" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB device write) before every timed step",
@@ -467,6 +482,7 @@ def main():
     ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
     ap.add_argument("--fused", action="store_true", help="with --dist: exchange fused into the scatter kernel")
+    ap.add_argument("--graph", action="store_true", help="replay hs_sort captured in a CUDA graph (small sizes)")
     args = ap.parse_args()
     import workload as W
     cfg = W.CONFIGS[args.config]

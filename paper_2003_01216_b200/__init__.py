@@ -22,7 +22,7 @@ __all__ = [
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
-    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan",
+    "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan", "SortGraph",
 ]
 
 HS_INT32, HS_INT64 = 0, 1
@@ -308,6 +308,39 @@ def hs_sort_pairs(keys, tags, num_digits: int, chunks_per_bucket: int = 8, strea
         _check(load().hs_sort_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, chunks_per_bucket,
                                     _stream(stream)))
     return keys, tags
+
+
+class SortGraph:
+    """hs_sort of one fixed device buffer captured once in a CUDA graph and
+    replayed: for launch-bound sizes (the ~30 kernel launches and the
+    stream-ordered scratch allocation of one call become one graph launch).
+    The library never synchronises the host inside a call, so the whole call
+    is capturable; scratch comes from graph memory nodes.
+
+        g = SortGraph(buf, num_digits=6)   # buf: CUDA tensor, sorted in place on every replay()
+        buf.copy_(new_keys); g.replay()
+    """
+
+    def __init__(self, keys, num_digits: int, chunks_per_bucket: int = 8):
+        torch = _torch()
+        _check_tensor(keys, "keys")
+        self.keys = keys
+        self.stream = torch.cuda.Stream(keys.device)
+        self.graph = torch.cuda.CUDAGraph()
+        self.stream.wait_stream(torch.cuda.current_stream(keys.device))
+        # one uncaptured call on a scratch copy first: the library's one-time
+        # per-device setup (kernel attributes, occupancy queries, memory pool
+        # threshold) must not run inside a capture
+        warm = keys.clone()
+        with torch.cuda.stream(self.stream):
+            hs_sort(warm, num_digits, chunks_per_bucket, stream=self.stream)
+        self.stream.synchronize()
+        del warm
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            hs_sort(keys, num_digits, chunks_per_bucket, stream=self.stream)
+
+    def replay(self) -> None:
+        self.graph.replay()
 
 
 class PartitionPlan:

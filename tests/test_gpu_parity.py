@@ -415,3 +415,16 @@ def test_max_size_int32():
     lo, hi = int(off[5]), int(off[6])
     bucket = keys[(keys // 10**8) == 5]
     assert_same(d[lo:hi].cpu().numpy(), np.sort(bucket), "bucket 5 at n = 2^31 - 1")
+
+
+def test_sort_graph_api():
+    """SortGraph: one capture, many replays on new data in the same buffer."""
+    buf = torch.empty(123_457, dtype=torch.int32, device=DEV)
+    g = None
+    for i in range(3):
+        keys = rand_keys(buf.numel(), 10**6, 500 + i, np.int32)
+        buf.copy_(torch.from_numpy(keys).to(DEV))
+        if g is None:
+            g = hs.SortGraph(buf, 6, 8)  # capture does not run the sort
+        g.replay()
+        assert_same(host(buf), O.sort(keys, 6, 8), f"replay {i}")
