@@ -1,9 +1,13 @@
 // k_merge.cu -- a5 (in-chunk merge levels) and a6 (the paper's binary-tree
 // merge of the chunks) as merge-path partitioned merge levels.
 //
-//   K6a k_merge_partition  co-rank search for every TM-aligned output boundary
+//   K6a k_merge_partition  co-rank search for every TM-aligned output boundary,
+//                          coarse phase on the previous generation's key
+//                          samples (L2), fine phase over ~64 keys in HBM
 //   K6b k_merge_level      persistent, double-buffered merge of every active
-//                          run pair of every bucket at one level
+//                          run pair of every bucket at one level; writes the
+//                          key samples of its output for the next level
+//   k_sample               samples of caller-given runs (hs_merge level 0)
 //   K7  k_copy             in-place hs_merge with an odd number of rounds
 //
 // K6b pipeline (per CTA, warp-specialised):
