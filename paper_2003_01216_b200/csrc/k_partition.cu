@@ -273,11 +273,11 @@ struct ScatSmem {
 
 // Rank + re-stage one tile held in `stage` (blocked: thread tid owns slots
 // tid*VT ..).  FULL: every slot is a key (interior tile) -> no validity tests.
-template <typename K, int NT, int VT, bool FULL>
+template <typename K, int NT, int VT, bool FULL, bool TABLE>
 __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__restrict__ sOut, uint8_t *sDig,
                                              K *__restrict__ out, int jlo, int jhi, int tile, const DigitParams<K> &dp,
                                              const Ctl *__restrict__ ctl, const uint32_t *__restrict__ tile_pref,
-                                             unsigned (*s_wtot)[5], int *s_dstart, K **s_dptr,
+                                             unsigned (*s_wtot)[5], int *s_dstart, int *s_delta, K **s_dptr,
                                              const DstTable<K> &dtab) {
     constexpr int E = 16 / sizeof(K);
     constexpr int NW = NT / 32;
@@ -362,7 +362,8 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
             s_dstart[lane] = (int)dstart;
             // global position of tile-local slot j of digit d = delta[d] + j (< 2^31)
             const long long delta = ctl->off[lane] + (long long)tile_pref[(size_t)tile * 10 + lane] - (long long)dstart;
-            s_dptr[lane] = (dtab.use ? dtab.dst[lane] - ctl->off[lane] : out) + delta;
+            if (TABLE) s_dptr[lane] = dtab.dst[lane] - ctl->off[lane] + delta;
+            else s_delta[lane] = (int)delta;  // < 2^31
         }
     }
     __syncthreads();
@@ -397,14 +398,15 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
     const int nvalid = jhi - jlo;
     for (int j = tid; j < nvalid; j += NT) {
         HS_DASSERT(sDig[j] < 10);
-        s_dptr[sDig[j]][j] = sOut[j];
+        if (TABLE) s_dptr[sDig[j]][j] = sOut[j];
+        else out[s_delta[sDig[j]] + j] = sOut[j];
     }
 }
 
 // Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the next
 // tile is prefetched by one 1-D bulk async copy into the other stage while
 // the current one is ranked and scattered.
-template <typename K, int NT, int VT>
+template <typename K, int NT, int VT, bool TABLE>
 __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *__restrict__ out, int n, int h,
                                                 DigitParams<K> dp, const Ctl *__restrict__ ctl,
                                                 const uint32_t *__restrict__ tile_pref, int ntiles, DstTable<K> dtab) {
@@ -418,7 +420,8 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ unsigned s_wtot[NW][5];
     __shared__ int s_dstart[10];
-    __shared__ K *s_dptr[10];
+    __shared__ K *s_dptr[TABLE ? 10 : 1];
+    __shared__ int s_delta[10];
     const int tid = threadIdx.x;
 
     // virtual tile t covers [t*T - h, (t+1)*T - h): 16-byte aligned in memory
@@ -449,11 +452,11 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
         const int jhi = (int)((long long)n - v0 < T ? (long long)n - v0 : (long long)T);
         const K *stage = stage0 + slot * T;
         if (jlo == 0 && jhi == T)
-            scatter_tile<K, NT, VT, true>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
-                                          s_dptr, dtab);
+            scatter_tile<K, NT, VT, true, TABLE>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot,
+                                                 s_dstart, s_delta, s_dptr, dtab);
         else
-            scatter_tile<K, NT, VT, false>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot, s_dstart,
-                                           s_dptr, dtab);
+            scatter_tile<K, NT, VT, false, TABLE>(stage, sOut, sDig, out, jlo, jhi, t, dp, ctl, tile_pref, s_wtot,
+                                                  s_dstart, s_delta, s_dptr, dtab);
         __syncthreads();  // stage / sOut / tables are reused next iteration
     }
 }
@@ -498,21 +501,23 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     }
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
-    auto kern = k_scatter<K, G::kScatNT, G::kScatVT>;
-    static int configured_dev = -1;
-    static int per_sm = 1;
+    // local CSR output, or the destination-pointer table of hs_partition_scatter
+    auto kern = dst10 ? k_scatter<K, G::kScatNT, G::kScatVT, true> : k_scatter<K, G::kScatNT, G::kScatVT, false>;
+    static int configured_dev[2] = {-1, -1};
+    static int per_sm[2] = {1, 1};
+    const int ki = dst10 ? 1 : 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured_dev != dev) {
+    if (configured_dev[ki] != dev) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::bytes());
         if (e != cudaSuccess) return e;
         int occ = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kScatNT, SS::bytes());
         if (e != cudaSuccess) return e;
-        per_sm = occ > 0 ? occ : 1;
-        configured_dev = dev;
+        per_sm[ki] = occ > 0 ? occ : 1;
+        configured_dev[ki] = dev;
     }
-    long long grid = (long long)per_sm * num_sms;
+    long long grid = (long long)per_sm[ki] * num_sms;
     if (grid > ntiles) grid = ntiles;
     prof_begin(kProfScatter, st);
     DstTable<K> dtab;
