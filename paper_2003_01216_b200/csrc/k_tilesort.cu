@@ -9,15 +9,19 @@
 //
 // K5 replaces the paper's per-thread sequential quicksort (Fig 1c, P:50,
 // P:62) -- a data-dependent, branchy, serial algorithm that maps badly onto
-// SIMT lanes -- by the GPU shape of the same "sort the partitions, then merge
-// sorted lists pairwise" idea its parallel sorts are built from:
-//   1. each thread sorts VT keys in registers (Batcher odd-even network,
-//      compile-time register indices, no branches; VT = 53 int32 / 27 int64 --
-//      a longer network is cheaper than one more shared-memory round);
-//   2. log2(NT) merge-path merge rounds in shared memory turn the NT sorted
-//      runs into one (the binary-tree merge of P:58-60 at CTA scope).
-// Keys-only data makes the sorted tile unique, so the (unstable) network
-// order is unobservable.
+// SIMT lanes.  Two paths, the same unique sorted tile:
+//   bucket pass (int32, the usual case): keys are split into 2 NT value
+//      ranges of the tile's [min, max], counted and scattered with shared-
+//      memory atomics, and each thread sorts its two buckets in registers;
+//      tiles spanning < 2 NT values become an exact counting sort;
+//   merge rounds (int64, and int32 tiles with a bucket over CAP keys): each
+//      thread sorts VT keys in registers (Batcher odd-even network,
+//      compile-time register indices; VT = 53 int32 / 27 int64), then
+//      log2(NT) merge-path merge rounds in shared memory turn the NT sorted
+//      runs into one -- the GPU shape of the paper's "sort the partitions,
+//      then merge sorted lists pairwise" at CTA scope.
+// Keys-only data makes the sorted tile unique, so neither path's (unstable)
+// order of equal keys is observable.
 #include <cstdint>
 
 #include "hs_device.cuh"
@@ -40,6 +44,18 @@
 #endif
 #ifndef HS_SORT_MINB64
 #define HS_SORT_MINB64 2
+#endif
+#ifndef HS_SORT_BUCKETS
+#define HS_SORT_BUCKETS 1  // int32: bucket pass (2 NT value buckets) before the merge-round fallback
+#endif
+#ifndef HS_SORT_CAP
+#define HS_SORT_CAP 48  // keys per bucket sorted in registers (mean T / 2NT = 26.5)
+#endif
+#ifndef HS_SORT_BUCKETS64
+#define HS_SORT_BUCKETS64 0
+#endif
+#ifndef HS_SORT_CAP64
+#define HS_SORT_CAP64 32
 #endif
 
 namespace hs {
@@ -102,6 +118,9 @@ __device__ __forceinline__ void bulk_s2g_ts(void *dst, const void *src, uint32_t
                  : "memory");
 }
 
+__device__ __forceinline__ float to_float_rz(uint32_t u) { return __uint2float_rz(u); }
+__device__ __forceinline__ float to_float_rz(unsigned long long u) { return __ull2float_rz(u); }
+
 template <typename K>
 __device__ __forceinline__ K lds_k(uint32_t a);
 template <>
@@ -124,7 +143,7 @@ struct TSGeo {
     static constexpr size_t bytes() { return (size_t)(T + 2 * E) * sizeof(K); }
 };
 
-template <typename K, int NT, int VT, int MINB>
+template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp) {
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
@@ -172,76 +191,185 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     const bool live0 = tid * VT < len;
 #pragma unroll
     for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
-    if (live0) oddeven_sort<VT>(v);
+    const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
+    K *const so = sbuf + sh;  // so[p] <-> out[p]
+    int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile); 2: bucket pass (scattered, buckets to sort)
+    uint32_t bk_base = 0, bk_c0 = 0, bk_c1 = 0;  // mode 2: my two buckets
 
-    // 3. merge rounds (R = threads per run).  Bitonic storage: in round R the
-    // input run q (length RL = R VT) is stored ascending if q is even (the
-    // pair's A) and DESCENDING if q is odd (the pair's B), so a pair occupies
-    // one bitonic stretch of shared memory.  A thread merges from both ends
-    // of what is left of it: the smaller of the two end keys is always the
-    // next output, even after one run is exhausted (the pointers then walk
-    // towards each other inside the other run), so the serial merge needs no
-    // bounds tests and no sentinels; ties take the A end (stable-left).
-    // Every thread stores every round (threads past the leaf's end hold
-    // kMax pads), so the stretch is complete; only threads with an output
-    // below len merge.
-    const uint32_t sm_u = smem_u32(sm);
-#pragma unroll 1
-    for (int lgR = 0; (1 << lgR) < NT; ++lgR) {
-        const int R = 1 << lgR, RL = R * VT;
-        const int q = tid >> lgR;  // this thread's outputs form part of input run q
-        __syncthreads();           // everyone has read the previous round's runs
-        if ((q & 1) == 0) {
+    if constexpr (BUCKETS > 0) {
+        // 2'. Bucket pass (the usual case).  Keys are split by value into
+        // BUCKETS equal-width ranges of the tile's [min, max] (a monotone
+        // float scaling, so bucket order is key order), counted and scattered
+        // into so[] with shared-memory atomics, and every thread sorts its two
+        // buckets in registers (a CAP-key network).  About 2 + 2/VT shared
+        // accesses per key instead of ~2.6 per merge round; the merge rounds
+        // below remain the path for tiles with a bucket over CAP keys (skew,
+        // heavy duplicates) -- the result is the same unique sorted tile.
+        static_assert(BUCKETS == 2 * NT, "two buckets per thread");
+        __shared__ uint32_t bcnt[BUCKETS];
+        __shared__ K red[2][NT / 32];
+        __shared__ uint32_t wsum[NT / 32];
+        using U = typename KeyTraits<K>::U;
+        const int lane = tid & 31, warp = tid >> 5;
+        K lmin = kMax, lmax = (K)(-kMax - 1);
 #pragma unroll
-            for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
-        } else {  // run q reversed in place: canonical c <-> (2q+1) RL - 1 - c
-            const int m = (2 * q + 1) * RL - 1 - tid * VT;
-#pragma unroll
-            for (int k = 0; k < VT; ++k) sm[m - k] = v[k];
-        }
-        __syncthreads();
-        if (tid * VT < len) {
-            const int j = tid & (2 * R - 1);
-            const int a0 = (tid - j) * VT, bE = a0 + 2 * RL;  // A = sm[a0, a0+RL) asc, B[k] = sm[bE-1-k]
-            const int diag = j * VT;
-            // merge path: first m with !(A[m] <= B[diag-1-m]); B[diag-1-m] = sm[bE - diag + m]
-            int l = diag - RL > 0 ? diag - RL : 0, r = diag < RL ? diag : RL;
-            const uint32_t ua = sm_u + (uint32_t)a0 * sizeof(K), ub = sm_u + (uint32_t)(bE - diag) * sizeof(K);
-            while (l < r) {
-                const int mid = (l + r) >> 1;
-                const bool pr = lds_k<K>(ua + mid * (int)sizeof(K)) <= lds_k<K>(ub + mid * (int)sizeof(K));
-                l = pr ? mid + 1 : l;
-                r = pr ? r : mid;
+        for (int k = 0; k < VT; ++k)
+            if (tid * VT + k < len) {
+                lmin = v[k] < lmin ? v[k] : lmin;
+                lmax = v[k] > lmax ? v[k] : lmax;
             }
-            uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
-            uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
-            HS_DASSERT(l >= 0 && l <= RL && diag - l >= 0 && diag - l <= RL && bE <= T);
-            [[maybe_unused]] const uint32_t lo_b = ua, hi_b = sm_u + (uint32_t)bE * sizeof(K);  // the pair's stretch
-            K x = lds_k<K>(pi), y = lds_k<K>(pj);
 #pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                const bool p = x <= y;
-                v[k] = p ? x : y;
-                if (k + 1 < VT) {
-                    pi += p ? (uint32_t)sizeof(K) : 0u;
-                    pj -= p ? 0u : (uint32_t)sizeof(K);
-                    HS_DASSERT(pi >= lo_b && pi < hi_b && pj >= lo_b && pj < hi_b);
-                    const K t = lds_k<K>(p ? pi : pj);
-                    x = p ? t : x;
-                    y = p ? y : t;
+        for (int o = 16; o >= 1; o >>= 1) {
+            const K a = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
+            lmin = a < lmin ? a : lmin;
+            lmax = c > lmax ? c : lmax;
+        }
+        if (lane == 0) {
+            red[0][warp] = lmin;
+            red[1][warp] = lmax;
+        }
+        bcnt[2 * tid] = 0;
+        bcnt[2 * tid + 1] = 0;
+        __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
+        K mn = red[0][0], mx = red[1][0];
+#pragma unroll
+        for (int w = 1; w < NT / 32; ++w) {
+            mn = red[0][w] < mn ? red[0][w] : mn;
+            mx = red[1][w] > mx ? red[1][w] : mx;
+        }
+        const U range = (U)mx - (U)mn;
+        if (range == 0) {  // constant tile: every order is the sorted one
+            for (int j = tid; j < len; j += NT) so[j] = mn;
+            mode = 1;
+        } else {
+            // range < BUCKETS: one bucket per key value (an exact counting sort,
+            // buckets need no sort and have no capacity limit)
+            const bool exact = range < (U)BUCKETS;
+            const float scale = (float)BUCKETS / ((float)range + 1.0f);
+            auto bucket_of_key = [&](K k) -> int {
+                const U u = (U)k - (U)mn;
+                if (exact) return (int)u;
+                const int bk = (int)(to_float_rz(u) * scale);  // monotone in k
+                return bk < BUCKETS - 1 ? bk : BUCKETS - 1;
+            };
+#pragma unroll
+            for (int k = 0; k < VT; ++k)
+                if (tid * VT + k < len) atomicAdd(&bcnt[bucket_of_key(v[k])], 1u);
+            __syncthreads();
+            const uint32_t c0 = bcnt[2 * tid], c1 = bcnt[2 * tid + 1];
+            if (!__syncthreads_or(!exact && (c0 > CAP || c1 > CAP))) {
+                // exclusive scan of the pair sums -> bucket starts (cursors)
+                uint32_t incl = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (lane == 31) wsum[warp] = incl;
+                __syncthreads();
+                uint32_t base = incl - (c0 + c1);
+                for (int w = 0; w < warp; ++w) base += wsum[w];
+                bcnt[2 * tid] = base;
+                bcnt[2 * tid + 1] = base + c0;
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < VT; ++k)
+                    if (tid * VT + k < len) so[atomicAdd(&bcnt[bucket_of_key(v[k])], 1u)] = v[k];
+                bk_base = base;
+                bk_c0 = c0;
+                bk_c1 = c1;
+                mode = exact ? 1 : 2;
+            }
+        }
+    }
+
+    if (mode == 2) {
+        // sort my two buckets in registers (v is dead on this path)
+        __syncthreads();
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t st = q == 0 ? bk_base : bk_base + bk_c0, cn = q == 0 ? bk_c0 : bk_c1;
+            if (cn > 1) {
+                K w[CAP];
+#pragma unroll
+                for (int i = 0; i < CAP; ++i) w[i] = i < (int)cn ? so[st + i] : kMax;
+                oddeven_sort<CAP>(w);
+#pragma unroll
+                for (int i = 0; i < CAP; ++i)
+                    if (i < (int)cn) so[st + i] = w[i];
+            }
+        }
+    } else if (mode == 0) {
+        if (live0) oddeven_sort<VT>(v);
+
+        // 3. merge rounds (R = threads per run).  Bitonic storage: in round R the
+        // input run q (length RL = R VT) is stored ascending if q is even (the
+        // pair's A) and DESCENDING if q is odd (the pair's B), so a pair occupies
+        // one bitonic stretch of shared memory.  A thread merges from both ends
+        // of what is left of it: the smaller of the two end keys is always the
+        // next output, even after one run is exhausted (the pointers then walk
+        // towards each other inside the other run), so the serial merge needs no
+        // bounds tests and no sentinels; ties take the A end (stable-left).
+        // Every thread stores every round (threads past the leaf's end hold
+        // kMax pads), so the stretch is complete; only threads with an output
+        // below len merge.
+        const uint32_t sm_u = smem_u32(sm);
+#pragma unroll 1
+        for (int lgR = 0; (1 << lgR) < NT; ++lgR) {
+            const int R = 1 << lgR, RL = R * VT;
+            const int q = tid >> lgR;  // this thread's outputs form part of input run q
+            __syncthreads();           // everyone has read the previous round's runs
+            if ((q & 1) == 0) {
+#pragma unroll
+                for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
+            } else {  // run q reversed in place: canonical c <-> (2q+1) RL - 1 - c
+                const int m = (2 * q + 1) * RL - 1 - tid * VT;
+#pragma unroll
+                for (int k = 0; k < VT; ++k) sm[m - k] = v[k];
+            }
+            __syncthreads();
+            if (tid * VT < len) {
+                const int j = tid & (2 * R - 1);
+                const int a0 = (tid - j) * VT, bE = a0 + 2 * RL;  // A = sm[a0, a0+RL) asc, B[k] = sm[bE-1-k]
+                const int diag = j * VT;
+                // merge path: first m with !(A[m] <= B[diag-1-m]); B[diag-1-m] = sm[bE - diag + m]
+                int l = diag - RL > 0 ? diag - RL : 0, r = diag < RL ? diag : RL;
+                const uint32_t ua = sm_u + (uint32_t)a0 * sizeof(K), ub = sm_u + (uint32_t)(bE - diag) * sizeof(K);
+                while (l < r) {
+                    const int mid = (l + r) >> 1;
+                    const bool pr = lds_k<K>(ua + mid * (int)sizeof(K)) <= lds_k<K>(ub + mid * (int)sizeof(K));
+                    l = pr ? mid + 1 : l;
+                    r = pr ? r : mid;
+                }
+                uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
+                uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
+                HS_DASSERT(l >= 0 && l <= RL && diag - l >= 0 && diag - l <= RL && bE <= T);
+                [[maybe_unused]] const uint32_t lo_b = ua, hi_b = sm_u + (uint32_t)bE * sizeof(K);  // the pair's stretch
+                K x = lds_k<K>(pi), y = lds_k<K>(pj);
+#pragma unroll
+                for (int k = 0; k < VT; ++k) {
+                    const bool p = x <= y;
+                    v[k] = p ? x : y;
+                    if (k + 1 < VT) {
+                        pi += p ? (uint32_t)sizeof(K) : 0u;
+                        pj -= p ? 0u : (uint32_t)sizeof(K);
+                        HS_DASSERT(pi >= lo_b && pi < hi_b && pj >= lo_b && pj < hi_b);
+                        const K t = lds_k<K>(p ? pi : pj);
+                        x = p ? t : x;
+                        y = p ? y : t;
+                    }
                 }
             }
         }
-    }
 
-    // 4. stage at the destination's 16-byte phase, bulk store the aligned middle
-    const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
-    K *const so = sbuf + sh;  // so[p] <-> out[p]
-    __syncthreads();
-    if (tid * VT < len) {
+        __syncthreads();
+        if (tid * VT < len) {
 #pragma unroll
-        for (int k = 0; k < VT; ++k) so[tid * VT + k] = v[k];
-    }
+            for (int k = 0; k < VT; ++k) so[tid * VT + k] = v[k];
+        }
+    }  // mode == 0
+
+    // 4. the sorted tile sits at the destination's 16-byte phase: bulk store the aligned middle
     fence_proxy_async_smem();
     __syncthreads();
     const int m0 = sh == 0 ? 0 : E - sh;            // first output at a 16-byte aligned address
@@ -266,10 +394,12 @@ struct SGeo;
 template <>
 struct SGeo<int32_t> {
     static constexpr int kNT = HS_SORT_NT, kVT = HS_SORT_VT, kMinB = HS_SORT_MINB;
+    static constexpr int kBuckets = HS_SORT_BUCKETS ? 2 * HS_SORT_NT : 0, kCap = HS_SORT_CAP;
 };
 template <>
 struct SGeo<int64_t> {
     static constexpr int kNT = HS_SORT_NT64, kVT = HS_SORT_VT64, kMinB = HS_SORT_MINB64;
+    static constexpr int kBuckets = HS_SORT_BUCKETS64 ? 2 * HS_SORT_NT64 : 0, kCap = HS_SORT_CAP64;
 };
 
 int sort_tile_keys(int dt) {
@@ -295,7 +425,7 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
                                cudaStream_t st) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
-    auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB>;
+    auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
