@@ -46,16 +46,19 @@
 #define HS_SORT_MINB64 2
 #endif
 #ifndef HS_SORT_BUCKETS
-#define HS_SORT_BUCKETS 1  // int32: bucket pass (2 NT value buckets) before the merge-round fallback
+#define HS_SORT_BUCKETS 2  // int32: buckets per thread of the bucket pass (0: merge rounds only)
 #endif
 #ifndef HS_SORT_CAP
 #define HS_SORT_CAP 48  // keys per bucket sorted in registers (mean T / 2NT = 26.5)
 #endif
 #ifndef HS_SORT_BUCKETS64
-#define HS_SORT_BUCKETS64 0
+#define HS_SORT_BUCKETS64 4  // int64: buckets per thread (16-bit packed counters)
+#endif
+#ifndef HS_SORT_BUNROLL
+#define HS_SORT_BUNROLL 1
 #endif
 #ifndef HS_SORT_CAP64
-#define HS_SORT_CAP64 32
+#define HS_SORT_CAP64 20  // mean T / 4NT = 6.75
 #endif
 
 namespace hs {
@@ -193,20 +196,24 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
     const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
     K *const so = sbuf + sh;  // so[p] <-> out[p]
-    int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile); 2: bucket pass (scattered, buckets to sort)
-    uint32_t bk_base = 0, bk_c0 = 0, bk_c1 = 0;  // mode 2: my two buckets
+    int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile / exact counting); 2: buckets to sort
+    constexpr int BPT_ = BUCKETS > 0 ? BUCKETS / NT : 1;
+    uint32_t bk_base = 0, bk_cnt[BPT_];  // mode 2: my buckets (set before mode becomes 2)
 
     if constexpr (BUCKETS > 0) {
         // 2'. Bucket pass (the usual case).  Keys are split by value into
         // BUCKETS equal-width ranges of the tile's [min, max] (a monotone
         // float scaling, so bucket order is key order), counted and scattered
-        // into so[] with shared-memory atomics, and every thread sorts its two
-        // buckets in registers (a CAP-key network).  About 2 + 2/VT shared
-        // accesses per key instead of ~2.6 per merge round; the merge rounds
-        // below remain the path for tiles with a bucket over CAP keys (skew,
-        // heavy duplicates) -- the result is the same unique sorted tile.
-        static_assert(BUCKETS == 2 * NT, "two buckets per thread");
-        __shared__ uint32_t bcnt[BUCKETS];
+        // into so[] with shared-memory atomics, and every thread sorts its BPT
+        // buckets in registers (a CAP-key network).  About 3 shared accesses
+        // per key instead of ~2.6 per merge round; the merge rounds below
+        // remain the path for tiles with a bucket over CAP keys (skew, heavy
+        // duplicates) -- the result is the same unique sorted tile.  PACK:
+        // two 16-bit counters per word (int64 tiles: leaves room for 2 CTAs/SM).
+        constexpr int BPT = BUCKETS / NT;
+        constexpr bool PACK = sizeof(K) == 8 || BPT > 2;
+        static_assert(BUCKETS == BPT * NT && (!PACK || BPT % 2 == 0), "bucket layout");
+        __shared__ uint32_t bcnt[PACK ? BUCKETS / 2 : BUCKETS];
         __shared__ K red[2][NT / 32];
         __shared__ uint32_t wsum[NT / 32];
         using U = typename KeyTraits<K>::U;
@@ -220,16 +227,16 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
             }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
-            const K a = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
-            lmin = a < lmin ? a : lmin;
+            const K x = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
+            lmin = x < lmin ? x : lmin;
             lmax = c > lmax ? c : lmax;
         }
         if (lane == 0) {
             red[0][warp] = lmin;
             red[1][warp] = lmax;
         }
-        bcnt[2 * tid] = 0;
-        bcnt[2 * tid + 1] = 0;
+#pragma unroll
+        for (int j = 0; j < (PACK ? BPT / 2 : BPT); ++j) bcnt[j * NT + tid] = 0;
         __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
         K mn = red[0][0], mx = red[1][0];
 #pragma unroll
@@ -252,14 +259,36 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 const int bk = (int)(to_float_rz(u) * scale);  // monotone in k
                 return bk < BUCKETS - 1 ? bk : BUCKETS - 1;
             };
+            // returns the bucket's count before this key (its slot when the counters hold starts)
+            auto bump = [&](int bk) -> uint32_t {
+                if (PACK) {
+                    const int sft = (bk & 1) * 16;
+                    return (atomicAdd(&bcnt[bk >> 1], 1u << sft) >> sft) & 0xFFFFu;
+                }
+                return atomicAdd(&bcnt[bk], 1u);
+            };
+            auto count_of = [&](int bk) -> uint32_t {
+                return PACK ? (bcnt[bk >> 1] >> ((bk & 1) * 16)) & 0xFFFFu : bcnt[bk];
+            };
 #pragma unroll
             for (int k = 0; k < VT; ++k)
-                if (tid * VT + k < len) atomicAdd(&bcnt[bucket_of_key(v[k])], 1u);
+                if (tid * VT + k < len) {
+                    const int bk = bucket_of_key(v[k]);
+                    if (PACK) atomicAdd(&bcnt[bk >> 1], 1u << ((bk & 1) * 16));  // no return: RED
+                    else atomicAdd(&bcnt[bk], 1u);
+                }
             __syncthreads();
-            const uint32_t c0 = bcnt[2 * tid], c1 = bcnt[2 * tid + 1];
-            if (!__syncthreads_or(!exact && (c0 > CAP || c1 > CAP))) {
-                // exclusive scan of the pair sums -> bucket starts (cursors)
-                uint32_t incl = c0 + c1;
+            uint32_t cnt[BPT], tot = 0;
+            bool over = false;
+#pragma unroll
+            for (int q = 0; q < BPT; ++q) {
+                cnt[q] = count_of(BPT * tid + q);
+                tot += cnt[q];
+                over |= cnt[q] > (uint32_t)CAP;
+            }
+            if (!__syncthreads_or(!exact && over)) {
+                // exclusive scan of the per-thread totals -> bucket starts (cursors)
+                uint32_t incl = tot;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
@@ -267,28 +296,42 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 }
                 if (lane == 31) wsum[warp] = incl;
                 __syncthreads();
-                uint32_t base = incl - (c0 + c1);
+                uint32_t base = incl - tot;
                 for (int w = 0; w < warp; ++w) base += wsum[w];
-                bcnt[2 * tid] = base;
-                bcnt[2 * tid + 1] = base + c0;
+                uint32_t st = base;
+                if (PACK) {
+#pragma unroll
+                    for (int q = 0; q < BPT; q += 2) {
+                        bcnt[(BPT * tid + q) >> 1] = st | ((st + cnt[q]) << 16);
+                        st += cnt[q] + cnt[q + 1];
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < BPT; ++q) {
+                        bcnt[BPT * tid + q] = st;
+                        st += cnt[q];
+                    }
+                }
                 __syncthreads();
 #pragma unroll
                 for (int k = 0; k < VT; ++k)
-                    if (tid * VT + k < len) so[atomicAdd(&bcnt[bucket_of_key(v[k])], 1u)] = v[k];
+                    if (tid * VT + k < len) so[bump(bucket_of_key(v[k]))] = v[k];
                 bk_base = base;
-                bk_c0 = c0;
-                bk_c1 = c1;
+#pragma unroll
+                for (int q = 0; q < BPT; ++q) bk_cnt[q] = cnt[q];
                 mode = exact ? 1 : 2;
             }
         }
     }
 
     if (mode == 2) {
-        // sort my two buckets in registers (v is dead on this path)
+        // sort my buckets in registers (v is dead on this path)
         __syncthreads();
-#pragma unroll 1
-        for (int q = 0; q < 2; ++q) {
-            const uint32_t st = q == 0 ? bk_base : bk_base + bk_c0, cn = q == 0 ? bk_c0 : bk_c1;
+        uint32_t st = bk_base;
+        constexpr int kBU = HS_SORT_BUNROLL;
+#pragma unroll kBU
+        for (int q = 0; q < BPT_; ++q) {
+            const uint32_t cn = bk_cnt[q];
             if (cn > 1) {
                 K w[CAP];
 #pragma unroll
@@ -298,6 +341,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 for (int i = 0; i < CAP; ++i)
                     if (i < (int)cn) so[st + i] = w[i];
             }
+            st += cn;
         }
     } else if (mode == 0) {
         if (live0) oddeven_sort<VT>(v);
@@ -394,12 +438,12 @@ struct SGeo;
 template <>
 struct SGeo<int32_t> {
     static constexpr int kNT = HS_SORT_NT, kVT = HS_SORT_VT, kMinB = HS_SORT_MINB;
-    static constexpr int kBuckets = HS_SORT_BUCKETS ? 2 * HS_SORT_NT : 0, kCap = HS_SORT_CAP;
+    static constexpr int kBuckets = HS_SORT_BUCKETS * HS_SORT_NT, kCap = HS_SORT_CAP;
 };
 template <>
 struct SGeo<int64_t> {
     static constexpr int kNT = HS_SORT_NT64, kVT = HS_SORT_VT64, kMinB = HS_SORT_MINB64;
-    static constexpr int kBuckets = HS_SORT_BUCKETS64 ? 2 * HS_SORT_NT64 : 0, kCap = HS_SORT_CAP64;
+    static constexpr int kBuckets = HS_SORT_BUCKETS64 * HS_SORT_NT64, kCap = HS_SORT_CAP64;
 };
 
 int sort_tile_keys(int dt) {
