@@ -135,6 +135,13 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
  * S:326-334): MSD partition -> sort each chunk -> tree-merge each bucket's
  * chunks.  Buckets land "to its place in the original array" because
  * each bucket's last merge level writes straight into keys.
+ * Sorting a chunk larger than one tile starts with one quicksort-style
+ * partition step with many pivots (K5a): the chunk is split by key value into
+ * equal-width sub-ranges of its bucket's digit range, each of which is then
+ * sorted in one shared-memory tile; a bucket whose sub-ranges overflow a tile
+ * (skewed keys, heavy duplicates) falls back to tile sort + in-chunk merge
+ * levels.  Either way the result is the unique ascending array.  The split
+ * is on unless the environment variable HS_SPLIT=0 is set (A/B measurements).
  *
  *   keys[n]            in/out: device; ascending on return.
  *   num_digits, chunks_per_bucket: as above.
@@ -245,8 +252,8 @@ int hs_tile_keys(hs_dtype_t dtype, int which /* 0 scatter, 1 tile sort, 2 merge 
  * on the launching stream.  hs_profile_read synchronises on them, writes
  * per-kind total milliseconds and launch counts for kinds [0, nkinds) and
  * forgets them; returns 0, or -1 if an event query failed.  Kind names:
- * hs_profile_kind_name(k), k = 0 .. 7 (tile_hist, tile_scan, scatter, plan,
- * tile_sort, merge_partition, merge_level, copy).
+ * hs_profile_kind_name(k), k = 0 .. 9 (tile_hist, tile_scan, scatter, plan,
+ * tile_sort, merge_partition, merge_level, copy, split_count, split_scatter).
  */
 int hs_profile_enable(int on);
 int hs_profile_read(double *ms, int *count, int nkinds);
@@ -260,6 +267,18 @@ const char *hs_profile_kind_name(int kind);
  */
 int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chunks_per_bucket, int mode,
                    int *levels_out, int *tile_levels_out);
+
+/*
+ * The device plan hs_sort would run on keys (bench / tests: which buckets the
+ * K5a value split takes, hence how many merge levels run).  Runs the
+ * partition and the split into scratch memory (keys is not modified),
+ * synchronises the stream and writes, per bucket b (host arrays of 10):
+ * levels_out[b] = merge levels L[b], split_out[b] = 1 if bucket b's chunks
+ * were value-split, leaves_out[b] = tile-sort leaves per chunk.  Arguments
+ * and errors as hs_sort.
+ */
+hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
+                         int32_t *levels_out, int32_t *split_out, int32_t *leaves_out, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

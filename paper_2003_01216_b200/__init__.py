@@ -19,7 +19,7 @@ from . import _build
 
 __all__ = [
     "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
-    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_host",
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_plan", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
     "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan", "SortGraph",
@@ -32,9 +32,10 @@ EXPORTED_SYMBOLS = (
     "hs_last_error_message", "hs_abi_version", "hs_last_launch_count", "hs_tile_keys",
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
     "hs_msd_partition_pairs", "hs_sort_pairs",
-    "hs_partition_plan_create", "hs_partition_scatter", "hs_partition_plan_destroy",
+    "hs_partition_plan_create", "hs_partition_scatter", "hs_partition_plan_destroy", "hs_sort_plan",
 )
-PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy")
+PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy",
+                 "split_count", "split_scatter")
 
 
 class HybridSortError(RuntimeError):
@@ -66,10 +67,11 @@ def load(path: str | None = None):
     lib.hs_merge.argtypes = [vp, vp, i64, ci, vp, ci, vp]
     lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
     lib.hs_sort_shared.argtypes = [vp, i64, ci, ci, vp]
+    lib.hs_sort_plan.argtypes = [vp, i64, ci, ci, ci, vp, vp, vp, vp]
     lib.hs_msd_partition_pairs.argtypes = [vp, vp, i64, ci, vp, vp, vp, vp]
     lib.hs_sort_pairs.argtypes = [vp, vp, i64, ci, ci, vp]
     for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared",
-              "hs_msd_partition_pairs", "hs_sort_pairs"):
+              "hs_msd_partition_pairs", "hs_sort_pairs", "hs_sort_plan"):
         getattr(lib, f).restype = ci
     lib.hs_status_string.argtypes = [ci]
     lib.hs_status_string.restype = ctypes.c_char_p
@@ -264,6 +266,22 @@ def hs_sort(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None, vali
     with torch.cuda.device(keys.device):
         _check(load().hs_sort(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket, _stream(stream)))
     return keys
+
+
+def hs_sort_plan(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None):
+    """The plan hs_sort would run on keys (keys unchanged): dict of per-bucket
+    merge levels, K5a split flags and tile-sort leaves per chunk."""
+    import numpy as np
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    dt = _dtype_code(keys)
+    L = np.zeros(10, dtype=np.int32)
+    sp = np.zeros(10, dtype=np.int32)
+    lv = np.zeros(10, dtype=np.int32)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort_plan(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket,
+                                   L.ctypes.data, sp.ctypes.data, lv.ctypes.data, _stream(stream)))
+    return {"levels": L.tolist(), "split": sp.tolist(), "leaves": lv.tolist()}
 
 
 def hs_sort_shared(keys, chunks: int = 8, stream=None):

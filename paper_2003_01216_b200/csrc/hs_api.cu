@@ -3,6 +3,7 @@
 // sequence of each entry point.  Every step of the method runs in the
 // kernels of hs_kernels.cu; this file only sequences them.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -123,11 +124,13 @@ struct Workspace {
     uint32_t *tile_pref = nullptr;
     int *corank = nullptr;
     void *samp[2] = {nullptr, nullptr};  // key samples (ping-pong by merge level)
+    uint32_t *sbtab = nullptr;           // K5a split table (sub-range starts) and cursors
+    uint32_t *sbcur = nullptr;
     size_t zero_bytes = 0;
 };
 
 hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
-                     size_t samp_bytes, cudaStream_t st) {
+                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
@@ -135,7 +138,8 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     size_t tp = round_up(ntiles * 10 * 4, 256);
     size_t k = round_up(corank_words * 4, 256);
     size_t sp = round_up(samp_bytes, 256);
-    size_t total = a + c + z + th + tp + k + 2 * sp;
+    size_t sw = round_up(split_words * 4, 256);
+    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -153,6 +157,10 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     if (samp_bytes) {
         w->samp[0] = b + a + c + z + th + tp + k;
         w->samp[1] = b + a + c + z + th + tp + k + sp;
+    }
+    if (split_words) {
+        w->sbtab = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp);
+        w->sbcur = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp + sw);
     }
     w->zero_bytes = c + z;
     return HS_OK;
@@ -217,7 +225,8 @@ cudaEvent_t prof_event() {
 }
 
 const char *const kProfNames[hs::kProfKinds] = {"tile_hist", "tile_scan", "scatter", "plan",
-                                                 "tile_sort", "merge_partition", "merge_level", "copy"};
+                                                 "tile_sort", "merge_partition", "merge_level", "copy",
+                                                 "split_count", "split_scatter"};
 
 }  // namespace
 
@@ -412,7 +421,7 @@ namespace {
 
 // a1-a7 on validated arguments (n > 0).  key_shift as partition_impl.
 hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
-                      int log2c, cudaStream_t stream, int *launches_out) {
+                      int log2c, cudaStream_t stream, int *launches_out, hs::Plan *inspect = nullptr) {
     hs_status_t s;
     int sms;
     cudaError_t e = device_setup(&sms);
@@ -426,10 +435,33 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     unsigned long long div, magic;
     digit_params(num_digits, key_shift ? HS_INT64 : dtype, &div, &magic);
 
+    // K5a value split of the chunks (on unless HS_SPLIT=0: A/B switch for measurements)
+    static const bool split_on = [] {
+        const char *e = getenv("HS_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    const long long split_words = split_on ? hs::split_table_words(n, log2c, T) : 0;
     Workspace ws;
-    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
-                      (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
+    if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
+                      (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words)) != HS_OK)
         return s;
+    if (inspect) {  // hs_sort_plan: partition + split into scratch, read the plan back
+        void *F = (char *)ws.S + round_up((size_t)n * ksize(dtype), 256);
+        cudaError_t e2 = cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream);
+        if (e2 == cudaSuccess)
+            e2 = hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                      ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift);
+        int dummy = 0;
+        if (e2 == cudaSuccess && split_on)
+            e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
+                                  &dummy, stream);
+        if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
+        cudaError_t fe = cudaFreeAsync(ws.base, stream);
+        if (e2 == cudaSuccess) e2 = fe;
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(stream);
+        if (e2 != cudaSuccess) return cuda_fail(e2, "hs_sort_plan");
+        return HS_OK;
+    }
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
@@ -438,8 +470,14 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                                      ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift),
                 "K1-K3 partition");
     launches += 2;
-    // a5: leaf-tile sort S -> (keys | S) per bucket parity
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
+    // a5 (K5a): value split of every chunk that exceeds one tile, S -> keys
+    if (split_on)
+        HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, ws.S, keys, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
+                                     key_shift, &launches, stream),
+                    "K5a split");
+    // a5: leaf-tile sort (S, or keys for split buckets) -> (keys | S) per bucket parity
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
+                                     ws.sbtab),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
@@ -476,6 +514,33 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     int launches = 0;
     if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) return s;
     g_launches = launches;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
+                         int32_t *levels_out, int32_t *split_out, int32_t *leaves_out, cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if (!levels_out || !split_out || !leaves_out) return fail(HS_ERR_INVALID_VALUE, "output array is NULL");
+    hs::Plan P;
+    memset(&P, 0, sizeof(P));
+    if (n > 0) {
+        int launches = 0;
+        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream,
+                           &launches, &P)) != HS_OK)
+            return s;
+    }
+    for (int b = 0; b < 10; ++b) {
+        levels_out[b] = n > 0 ? P.L[b] : 0;
+        split_out[b] = P.split[b];
+        leaves_out[b] = P.split[b] ? P.nsb[b] : (1 << P.k[b]);
+    }
+    g_launches = 0;
     g_err[0] = 0;
     return HS_OK;
 }

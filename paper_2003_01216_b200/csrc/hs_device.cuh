@@ -90,13 +90,32 @@ __device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &
 //    merges of a5; levels k[b] .. k[b]+log2 c - 1 are the paper's tree merge
 //    of the chunks (a6).
 //  * L[b] = number of merge levels this call runs for bucket b.
+//  * split[b] = 1 (hs_sort, K5a): every chunk of bucket b was split by key
+//    value into nsb[b] sub-ranges, each at most T keys; the tile-sort leaves
+//    are those sub-ranges (bounds in the split table at sboff[b]), k[b] = 0
+//    and the merge levels are only the paper's chunk tree (L[b] = log2 c).
 struct Plan {
     long long off[11];
-    long long tile_prefix[11];  // exclusive prefix of leaf counts (c << k[b])
+    long long tile_prefix[11];  // exclusive prefix of tile-sort leaf counts (c << k[b], or c * nsb[b])
+    long long sboff[10];        // split table: chunk j of bucket b owns [sboff + j (nsb+1), ... + nsb]
     int k[10];
     int L[10];
+    int split[10];
+    int nsb[10];
     int log2c;
     int Lmax;
+};
+
+// K5a bookkeeping (value split of the chunks), written by k_split_setup.
+struct SplitCfg {
+    long long slice_prefix[11];  // CTAs of the count / scatter passes per bucket (c * spc[b])
+    long long lo[10];            // bucket b's value range starts at b * 10^(D-1)
+    unsigned long long mul[10];  // sub-range of x = mulhi(x - lo, mul), mul = floor((2^w - 1) / 10^(D-1)) nsb[b]
+    int spc[10];                 // slices per chunk
+    int cand[10];                // bucket b is split if no sub-range of its chunks exceeds T
+    unsigned bad;                // buckets with an over-full sub-range (fall back to merge levels)
+    unsigned ticket;
+    int shift;                   // sort key of an item = item >> shift (hs_sort_pairs)
 };
 
 enum PlanMode { kPlanSort = 0, kPlanChunks = 1, kPlanMerge = 2 };
@@ -122,6 +141,9 @@ __device__ inline void compute_plan(Plan *P, const long long *off, int log2c, in
         }
         int L = (mode == kPlanSort) ? k + log2c : (mode == kPlanChunks ? k : log2c);
         P->off[b] = off[b];
+        P->split[b] = 0;
+        P->nsb[b] = 0;
+        P->sboff[b] = 0;
         P->k[b] = k;
         P->L[b] = L;
         P->tile_prefix[b] = acc;
@@ -212,6 +234,7 @@ struct Ctl {
     unsigned int ticket;
     long long off[11];
     Plan plan;
+    SplitCfg split;
 };
 
 // --------------------------------------------------------------- PTX glue

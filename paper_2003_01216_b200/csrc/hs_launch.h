@@ -14,7 +14,7 @@ struct Plan;
 // Optional per-kernel CUDA-event timing (hs_profile_enable); kinds match
 // hs_profile_kind_name().  No-ops unless enabled on the calling thread.
 enum ProfKind { kProfTileHist = 0, kProfTileScan, kProfScatter, kProfPlan, kProfTileSort, kProfMergePartition,
-                kProfMergeLevel, kProfCopy, kProfKinds };
+                kProfMergeLevel, kProfCopy, kProfSplitCount, kProfSplitScatter, kProfKinds };
 void prof_begin(int kind, cudaStream_t st);
 void prof_end(int kind, cudaStream_t st);
 
@@ -31,8 +31,18 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
                              int key_shift = 0, bool do_count = true, void *const *dst10 = nullptr);
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
+// sbtab: K5a split table (leaves of split buckets; null when no bucket can be split)
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
-                             long long max_tiles, cudaStream_t st);
+                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr);
+
+// K5a (k_split.cu): value split of every chunk of the buckets whose chunks
+// exceed one tile: setup (1 thread), count pass over S, per-chunk scan +
+// plan finalisation, scatter pass S -> F.  tab / cur hold tab_words words
+// (zeroed by the caller before the count pass).  Returns the kernels launched.
+long long split_table_words(long long n, int log2c, int tile_keys);
+cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, int *launches,
+                         cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
 // the samples this level writes for the next one (may be null).
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,

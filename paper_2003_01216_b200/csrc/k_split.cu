@@ -1,0 +1,359 @@
+// k_split.cu -- K5a: value split of each chunk before its tile sort (hs_sort).
+//
+// a5 sorts every chunk of every bucket ("sort the partitions",
+// the paper's per-thread quicksort).  A chunk of C3 holds 3.4M keys, far more
+// than one shared-memory tile (T = 27,136), so without this step K5 sorts
+// T-key leaves and log2(chunk / T) in-chunk merge levels (K6) rebuild the
+// chunk -- 7 full read+write passes over the array on C3.  K5a instead does
+// what one quicksort partition step does, with nsb - 1 pivots at once: the
+// chunk's keys are split by value into nsb equal-width sub-ranges of the
+// bucket's range [b 10^(D-1), (b+1) 10^(D-1)) (nsb = ceil(chunk / 0.9 T)),
+// so every sub-range is a leaf that K5 sorts in one tile and the sorted
+// sub-ranges, laid end to end, ARE the sorted chunk.  What remains of K6 is
+// the paper's binary tree merge of the c sorted chunks (a6).
+//
+//   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
+//                    offsets; zeroes the count table
+//   k_split_pass<0>  count: every CTA reads one slice (<= NT*VT keys) of one
+//                    chunk from S, counts its sub-ranges in shared memory and
+//                    adds the non-zero counts to the chunk's table row
+//   k_split_plan     one CTA per chunk: exclusive scan of the row -> sub-range
+//                    starts (+ cursor copy); a sub-range over T keys marks the
+//                    bucket "bad"; the last CTA finalises the Plan: split
+//                    buckets get k = 0, L = log2 c, leaves = sub-ranges; bad
+//                    buckets keep the tile + in-chunk merge plan (skewed keys,
+//                    heavy duplicates: correct either way, only slower)
+//   k_split_pass<1>  scatter: the slice is counted again, every non-empty
+//                    sub-range claims its output span with one global atomic,
+//                    the keys are staged by sub-range in shared memory and
+//                    written out run by run (coalesced within a sub-range)
+//
+// The order of keys inside a sub-range depends on atomic arrival order; the
+// tile sort that follows makes the result the unique sorted chunk (keys only;
+// hs_sort_pairs sorts unique (key << 32 | index) items, so stays stable).
+// Sub-range of a key: floor((x - lo_b) * nsb / 10^(D-1)) in fp32, clamped to
+// [0, nsb) -- a monotone function of the key (int -> float rounding, scaling
+// by a positive constant and truncation are all monotone), so sub-range order
+// is key order; keys clamped into bucket 0 / 9 (P:78 reading #3) land in the
+// first / last sub-range.  Roofline: HBM, 4 B read (count) + 8 B read+write
+// (scatter) per int32 key.
+#include <cstdint>
+
+#include "hs_device.cuh"
+#include "hs_launch.h"
+
+namespace hs {
+
+template <typename K>
+struct SplGeo;
+template <>
+struct SplGeo<int32_t> {
+    static constexpr int NT = 512, VT = 16, MINB_COUNT = 4, MINB_SCAT = 2;
+};
+template <>
+struct SplGeo<int64_t> {
+    static constexpr int NT = 512, VT = 8, MINB_COUNT = 4, MINB_SCAT = 2;
+};
+constexpr int kSplitMaxSub = 4096;  // sub-ranges per chunk (shared-memory counters)
+constexpr int kSplitPlanNT = 512;
+
+__host__ __device__ __forceinline__ long long split_target(int tile_keys) { return (long long)tile_keys * 9 / 10; }
+
+// ------------------------------------------------------------------ setup
+__global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, int key_shift, int tile_keys,
+                              int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab) {
+    __shared__ long long s_words;
+    if (threadIdx.x == 0) {
+        Plan &P = ctl->plan;
+        SplitCfg &C = ctl->split;
+        const long long c = 1LL << P.log2c, target = split_target(tile_keys);
+        long long acc_s = 0, acc_t = 0;
+        for (int b = 0; b < 10; ++b) {
+            const long long m = P.off[b + 1] - P.off[b], cm = (m + c - 1) / c;
+            const long long ns = (cm + target - 1) / target;
+            // ns <= div: the multiplier below fits the key width (and narrower sub-ranges would be empty)
+            const bool cand = P.k[b] > 0 && ns >= 2 && ns <= nsb_cap && (unsigned long long)ns <= div &&
+                              acc_t + c * (ns + 1) <= tab_cap;
+            C.cand[b] = cand;
+            C.slice_prefix[b] = acc_s;
+            if (cand) {
+                const long long spc = (cm + slice_keys - 1) / slice_keys;
+                C.spc[b] = (int)spc;
+                acc_s += c * spc;
+                P.nsb[b] = (int)ns;
+                P.sboff[b] = acc_t;
+                acc_t += c * (ns + 1);
+                C.lo[b] = (long long)b * (long long)div;
+                const unsigned long long wmax = key_bits == 32 ? 0xFFFFFFFFull : ~0ull;
+                C.mul[b] = wmax / div * (unsigned long long)ns;  // <= wmax since ns <= div
+            } else {
+                C.spc[b] = 1;
+                C.lo[b] = 0;
+                C.mul[b] = 0;
+            }
+        }
+        C.slice_prefix[10] = acc_s;
+        C.shift = key_shift;
+        s_words = acc_t;
+    }
+    __syncthreads();
+    for (long long q = threadIdx.x; q < s_words; q += blockDim.x) tab[q] = 0;
+}
+
+// ------------------------------------------------------------------ helpers
+// Sub-range of key k in its bucket: d = x - lo (x = k >> shift) and
+// t = min(mulhi(d, mul), ns - 1), t = 0 for d < 0 -- non-decreasing in k, and
+// t < ns for 0 <= d < 10^(D-1) (mul <= (2^w - 1) ns / 10^(D-1)).  int32: a key
+// of bucket b >= 1 has x >= b 10^(D-1) = lo and bucket 0 has lo = 0, so
+// x - lo never overflows.
+__device__ __forceinline__ int sub_range_of(int32_t k, int, long long lo, unsigned long long mul, int ns) {
+    const int32_t d = k - (int32_t)lo;
+    const int t = d < 0 ? 0 : (int)__umulhi((uint32_t)d, (uint32_t)mul);
+    return t < ns ? t : ns - 1;
+}
+__device__ __forceinline__ int sub_range_of(int64_t k, int shift, long long lo, unsigned long long mul, int ns) {
+    const long long d = (k >> shift) - lo;  // arithmetic shift: the sign of the key survives
+    const long long t = d < 0 ? 0 : (long long)__umul64hi((unsigned long long)d, mul);
+    return t < ns ? (int)t : ns - 1;
+}
+
+// In-place exclusive scan of a[0, n) by the whole CTA (NT threads, contiguous
+// segments per thread).  Ends with a barrier.
+template <int NT>
+__device__ __forceinline__ void cta_excl_scan(uint32_t *a, int n, uint32_t *wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int E = (n + NT - 1) / NT;
+    const int b0 = tid * E < n ? tid * E : n, b1 = b0 + E < n ? b0 + E : n;
+    uint32_t sum = 0;
+    for (int q = b0; q < b1; ++q) sum += a[q];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t base = incl - sum;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    for (int q = b0; q < b1; ++q) {
+        const uint32_t t = a[q];
+        a[q] = base;
+        base += t;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------- count / scatter
+// One CTA = one slice of <= NT*VT keys of one chunk.  All VT loads are issued
+// before any use (memory-level parallelism); the shared-memory histogram
+// gives every key its rank among the slice's keys of its sub-range.
+//   count:   the non-zero histogram entries are added to the chunk's row.
+//   scatter: one global atomic per non-empty sub-range claims the slice's
+//            span (issued before the local scan, so its latency overlaps
+//            it); keys are staged at their slice-local sorted position with
+//            their destination, then written in staged order -- consecutive
+//            threads write consecutive addresses within a sub-range.
+template <typename K, int NT, int VT, int MINB, bool SCAT>
+__global__ void __launch_bounds__(NT, MINB) k_split_pass(const Ctl *__restrict__ ctl, const K *__restrict__ S,
+                                                         K *__restrict__ F, uint32_t *tab, uint32_t *cur,
+                                                         int nsb_cap) {
+    constexpr int TS = NT * VT;
+    constexpr int QMAX = (kSplitMaxSub + NT - 1) / NT;
+    static_assert(TS <= 65536, "ranks are packed in 16 bits");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint32_t wsum[NT / 32];
+    uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap]
+    uint32_t *const gb = hist + nsb_cap;                              // SCAT: [nsb_cap] span starts
+    K *const skeys = reinterpret_cast<K *>(smem_raw + (((size_t)2 * nsb_cap * 4 + 15) & ~(size_t)15));
+    uint32_t *const sdst = reinterpret_cast<uint32_t *>(skeys + TS);
+    const Plan &P = ctl->plan;
+    const SplitCfg &C = ctl->split;
+    const int tid = threadIdx.x;
+
+    const long long g = blockIdx.x;
+    if (g >= C.slice_prefix[10]) return;
+    int b = 0;
+    while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
+    if (SCAT && !P.split[b]) return;  // bucket fell back to the merge plan: its keys stay in S
+    const long long r = g - C.slice_prefix[b];
+    const int spc = C.spc[b];
+    const long long j = r / spc, s = r - j * spc;
+    const long long m = P.off[b + 1] - P.off[b];
+    const long long c0 = part_start(m, P.log2c, j), c1 = part_start(m, P.log2c, j + 1);
+    const long long a0 = s * TS;
+    if (a0 >= c1 - c0) return;
+    const int cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
+    const long long cs = P.off[b] + c0;  // chunk start (absolute)
+    const K *in = S + cs + a0;
+    const int ns = P.nsb[b];
+    const long long lo = C.lo[b];
+    const unsigned long long mul = C.mul[b];
+    const int shift = C.shift;
+    HS_DASSERT(ns >= 2 && ns <= nsb_cap);
+
+    for (int q = tid; q < ns; q += NT) hist[q] = 0;
+    K v[VT];
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+        const int idx = k * NT + tid;
+        v[k] = idx < cnt ? in[idx] : K(0);
+    }
+    __syncthreads();
+    uint32_t tr[VT];  // sub-range << 16 | rank within the slice's keys of that sub-range
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+        if (k * NT + tid < cnt) {
+            const int t = sub_range_of(v[k], shift, lo, mul, ns);
+            if constexpr (SCAT) tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+            else atomicAdd(&hist[t], 1u);
+        }
+    }
+    __syncthreads();
+    const long long row = P.sboff[b] + j * (ns + 1);
+    if constexpr (!SCAT) {
+        for (int q = tid; q < ns; q += NT) {
+            const uint32_t h = hist[q];
+            if (h) atomicAdd(&tab[row + q], h);
+        }
+    } else {
+        uint32_t span[QMAX];
+#pragma unroll
+        for (int i = 0; i < QMAX; ++i) {
+            const int q = tid + i * NT;
+            if (q < ns) {
+                const uint32_t h = hist[q];
+                span[i] = h ? atomicAdd(&cur[row + q], h) : 0u;  // chunk-relative start of this slice's span
+            }
+        }
+        cta_excl_scan<NT>(hist, ns, wsum);  // hist -> slice-local starts (overlaps the atomics)
+#pragma unroll
+        for (int i = 0; i < QMAX; ++i) {
+            const int q = tid + i * NT;
+            if (q < ns) gb[q] = span[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {
+            if (k * NT + tid < cnt) {
+                const uint32_t t = tr[k] >> 16, rk = tr[k] & 0xFFFFu;
+                const uint32_t p = hist[t] + rk;
+                skeys[p] = v[k];
+                sdst[p] = gb[t] + rk;
+            }
+        }
+        __syncthreads();
+        K *const oc = F + cs;
+        for (int p = tid; p < cnt; p += NT) oc[sdst[p]] = skeys[p];
+    }
+}
+
+// ------------------------------------------------------------- per-chunk scan
+__global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t *tab, uint32_t *cur, int tile_keys) {
+    __shared__ uint32_t wsum[kSplitPlanNT / 32];
+    __shared__ bool s_last;
+    Plan &P = ctl->plan;
+    SplitCfg &C = ctl->split;
+    const int tid = threadIdx.x;
+    const int lg = P.log2c;
+    const int b = blockIdx.x >> lg;
+    const long long j = blockIdx.x & ((1 << lg) - 1);
+    if (b < 10 && C.cand[b]) {
+        const int ns = P.nsb[b];
+        uint32_t *row = tab + P.sboff[b] + j * (ns + 1);
+        uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
+        bool over = false;
+        for (int q = tid; q < ns; q += kSplitPlanNT) over |= row[q] > (uint32_t)tile_keys;
+        if (__syncthreads_or(over) && tid == 0) atomicOr(&C.bad, 1u << b);
+        cta_excl_scan<kSplitPlanNT>(row, ns, wsum);
+        for (int q = tid; q < ns; q += kSplitPlanNT) crow[q] = row[q];
+        if (tid == 0) {
+            const long long m = P.off[b + 1] - P.off[b];
+            const long long len = part_start(m, lg, j + 1) - part_start(m, lg, j);
+            row[ns] = (uint32_t)len;
+            HS_DASSERT(ns < 1 || row[ns - 1] <= (uint32_t)len);
+        }
+    }
+    // the last CTA to finish turns the candidates without an over-full
+    // sub-range into split buckets and re-derives the leaf prefix
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&C.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    const unsigned bad = *(volatile unsigned *)&C.bad;
+    const long long c = 1LL << lg;
+    long long acc = 0;
+    int lmax = 0;
+    for (int bb = 0; bb < 10; ++bb) {
+        const int sp = C.cand[bb] && !((bad >> bb) & 1u);
+        P.split[bb] = sp;
+        if (sp) {
+            P.k[bb] = 0;
+            P.L[bb] = lg;  // only the chunk tree (a6) remains
+        }
+        P.tile_prefix[bb] = acc;
+        acc += sp ? c * P.nsb[bb] : (c << P.k[bb]);
+        lmax = P.L[bb] > lmax ? P.L[bb] : lmax;
+    }
+    P.tile_prefix[10] = acc;
+    P.Lmax = lmax;
+}
+
+// ------------------------------------------------------------------ host
+long long split_table_words(long long n, int log2c, int tile_keys) {
+    return n / split_target(tile_keys) + 40 * (1LL << log2c) + 64;
+}
+
+static int nsb_bound(long long n, int log2c, int tile_keys) {
+    const long long c = 1LL << log2c, cm = (n + c - 1) / c, t = split_target(tile_keys);
+    const long long ns = (cm + t - 1) / t;
+    return (int)(ns < kSplitMaxSub ? (ns < 2 ? 2 : ns) : kSplitMaxSub);
+}
+
+template <typename K>
+static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uint32_t *cur, long long tab_words,
+                                  long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
+                                  int *launches, cudaStream_t st) {
+    using G = SplGeo<K>;
+    constexpr int TS = G::NT * G::VT;
+    const int nsb_cap = nsb_bound(n, log2c, tile_keys);
+    const size_t sm_count = (size_t)nsb_cap * 4;
+    const size_t sm_scat = (((size_t)2 * nsb_cap * 4 + 15) & ~(size_t)15) + (size_t)TS * (sizeof(K) + 4);
+    auto kc = k_split_pass<K, G::NT, G::VT, G::MINB_COUNT, false>;
+    auto ks = k_split_pass<K, G::NT, G::VT, G::MINB_SCAT, true>;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat)) != cudaSuccess)
+        return e;
+    const long long c = 1LL << log2c;
+    const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
+    prof_begin(kProfPlan, st);
+    k_split_setup<<<1, 1024, 0, st>>>(ctl, div, 8 * (int)sizeof(K), key_shift, tile_keys, TS, tab_words, nsb_cap,
+                                      tab);
+    prof_end(kProfPlan, st);
+    prof_begin(kProfSplitCount, st);
+    kc<<<(unsigned)grid, G::NT, sm_count, st>>>(ctl, S, F, tab, cur, nsb_cap);
+    prof_end(kProfSplitCount, st);
+    prof_begin(kProfPlan, st);
+    k_split_plan<<<(unsigned)(10 * c), kSplitPlanNT, 0, st>>>(ctl, tab, cur, tile_keys);
+    prof_end(kProfPlan, st);
+    prof_begin(kProfSplitScatter, st);
+    ks<<<(unsigned)grid, G::NT, sm_scat, st>>>(ctl, S, F, tab, cur, nsb_cap);
+    prof_end(kProfSplitScatter, st);
+    *launches += 4;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, int *launches,
+                         cudaStream_t st) {
+    return dt == 0 ? launch_split_t<int32_t>(ctl, (const int32_t *)S, (int32_t *)F, tab, cur, tab_words, n, log2c,
+                                             tile_keys, div, key_shift, launches, st)
+                   : launch_split_t<int64_t>(ctl, (const int64_t *)S, (int64_t *)F, tab, cur, tab_words, n, log2c,
+                                             tile_keys, div, key_shift, launches, st);
+}
+
+}  // namespace hs

@@ -148,7 +148,7 @@ struct TSGeo {
 
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
-                                                        K *samp) {
+                                                        K *samp, const uint32_t *__restrict__ sbtab) {
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
@@ -168,8 +168,19 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     int b = 0;
     while (b < 9 && g >= P.tile_prefix[b + 1]) ++b;
     const long long i = g - P.tile_prefix[b];
-    const long long lo = leaf_start(P, b, i);
-    const int len = (int)(leaf_start(P, b, i + 1) - lo);
+    long long lo;
+    int len;
+    if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (already in F)
+        const int ns = P.nsb[b];
+        const long long j = i / ns, t = i - j * ns;
+        const uint32_t *e = sbtab + P.sboff[b] + j * (ns + 1) + t;
+        lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
+        len = (int)(__ldg(e + 1) - __ldg(e));
+        src = F;
+    } else {
+        lo = leaf_start(P, b, i);
+        len = (int)(leaf_start(P, b, i + 1) - lo);
+    }
     if (len == 0) return;
     HS_DASSERT(len > 0 && len <= T && lo >= P.off[b] && lo + len <= P.off[b + 1]);
     K *const out = ((P.L[b] & 1) ? S : F) + lo;  // where this bucket's merge level 0 reads
@@ -466,7 +477,7 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
-                               cudaStream_t st) {
+                               cudaStream_t st, const uint32_t *sbtab) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
@@ -480,15 +491,15 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
-    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp);
+    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab);
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
-                             long long max_tiles, cudaStream_t st) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st);
+                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab);
 }
 
 }  // namespace hs

@@ -1,0 +1,179 @@
+"""K5a value split of the chunks (hs_sort): parity on inputs built to take
+the split, to fall back from it, and to mix both within one call.
+
+A bucket is split when its chunks exceed one tile (T keys); a split bucket
+whose equal-width value sub-ranges overflow a tile (skew, heavy duplicates,
+clamped keys piling into the first / last sub-range) falls back to tile sort
++ in-chunk merge levels.  Either way hs_sort must return the unique
+ascending array, so every case compares with the oracle element by element;
+``hs_sort_plan`` shows which path each bucket took, so the cases provably
+cover both.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workload as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2003_01216_b200 as hs  # noqa: E402
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    hs.load()
+
+
+def T(code):
+    return hs.tile_keys(code, 1)
+
+
+def run(keys, D, c):
+    d = torch.from_numpy(np.ascontiguousarray(keys)).to(DEV)
+    plan = hs.hs_sort_plan(d, D, c)
+    before = d.clone()
+    hs.hs_sort(d, D, c)
+    torch.cuda.synchronize()
+    return d.cpu().numpy(), plan, before
+
+
+def check(keys, D, c):
+    got, plan, _ = run(keys, D, c)
+    ref = O.sort(keys, D, c)
+    if not np.array_equal(got, ref):
+        bad = np.nonzero(got != ref)[0]
+        raise AssertionError(f"{bad.size} mismatches, first at {bad[0]}: got {got[bad[0]]} want {ref[bad[0]]}")
+    return plan
+
+
+def buckets(per_bucket, D, seed, dtype=np.int32, lo_frac=0.0, hi_frac=1.0):
+    """per_bucket[b] keys uniform over [lo_frac, hi_frac) of digit b's range, shuffled."""
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(seed)
+    parts = []
+    for b, m in enumerate(per_bucket):
+        lo = b * div + int(lo_frac * div)
+        hi = b * div + max(int(hi_frac * div), int(lo_frac * div) + 1)
+        parts.append(rng.integers(lo, hi, size=m, dtype=np.int64))
+    k = np.concatenate(parts).astype(dtype)
+    rng.shuffle(k)
+    return k
+
+
+@pytest.mark.parametrize("c", [1, 2, 8])
+def test_split_uniform_all_buckets(c):
+    t = T(0)
+    keys = buckets([c * 3 * t + 17 * b for b in range(10)], 9, 11 + c)
+    plan = check(keys, 9, c)
+    lg = c.bit_length() - 1
+    assert plan["split"] == [1] * 10
+    assert plan["levels"] == [lg] * 10          # only the paper's chunk tree remains
+    assert all(lv >= 2 for lv in plan["leaves"])
+
+
+def test_split_just_over_one_tile():
+    t = T(0)
+    keys = buckets([t + 1 + b for b in range(10)], 6, 5)   # c = 1: every chunk = T + 1 + b keys -> 2 sub-ranges
+    plan = check(keys, 6, 1)
+    assert plan["split"] == [1] * 10 and plan["leaves"] == [2] * 10
+
+
+def test_split_mixed_with_fallback_buckets():
+    """Buckets 1, 4, 7 split; 2 (one value), 5 (narrow peak), 9 (clamped keys) fall back; 0, 3 fit a tile."""
+    t, D, c = T(0), 7, 2
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(3)
+    m = 5 * t
+    parts = [
+        rng.integers(0, div, size=t // 3),                     # bucket 0: small, no split needed
+        rng.integers(div, 2 * div, size=m),                    # bucket 1: split
+        np.full(m, 2 * div + 12345),                           # bucket 2: constant -> over-full sub-range
+        rng.integers(3 * div, 4 * div, size=t // 2),           # bucket 3: small
+        rng.integers(4 * div, 5 * div, size=m + 999),          # bucket 4: split
+        5 * div + rng.integers(0, 1000, size=m),               # bucket 5: all in the first sub-range
+        rng.integers(7 * div, 8 * div, size=m - 5),            # bucket 7: split (bucket 6 empty)
+        rng.integers(10 * div, 2**31 - 1, size=m),             # bucket 9: clamped (>= 10^D): last sub-range
+    ]
+    keys = np.concatenate(parts).astype(np.int32)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert [plan["split"][b] for b in (1, 4, 7)] == [1, 1, 1]
+    assert [plan["split"][b] for b in (0, 2, 3, 5, 6, 9)] == [0] * 6
+    assert plan["levels"][1] == 1 and plan["levels"][2] > 1    # fallback keeps its in-chunk levels
+
+
+def test_split_clamped_and_negative_inside_split_buckets():
+    """A few clamped keys (negative -> bucket 0, >= 10^D -> bucket 9) land in the edge sub-ranges."""
+    t, D, c = T(0), 8, 2
+    keys = buckets([c * 4 * t] * 10, D, 21)
+    rng = np.random.default_rng(22)
+    idx = rng.choice(keys.size, 4000, replace=False)
+    keys[idx[:2000]] = -rng.integers(1, 2**31 - 1, size=2000)
+    keys[idx[2000:]] = rng.integers(10**D, 2**31 - 1, size=2000)
+    keys[idx[:5]] = np.iinfo(np.int32).min
+    keys[idx[-5:]] = np.iinfo(np.int32).max
+    plan = check(keys, D, c)
+    assert plan["split"][0] == 1 and plan["split"][9] == 1
+
+
+def test_split_sorted_and_reversed_input():
+    t = T(0)
+    n = 10 * 2 * 3 * t
+    for keys in (np.arange(n, dtype=np.int32) * 13, (np.arange(n, dtype=np.int32) * 13)[::-1].copy()):
+        D = len(str(int(keys.max())))
+        check(keys, D, 2)
+
+
+def test_split_duplicates_half_the_keys():
+    t, c = T(0), 4
+    keys = buckets([c * 3 * t] * 10, 9, 31)
+    keys[::2] = 123_456_789      # half of everything is one value in bucket 1
+    plan = check(keys, 9, c)
+    assert plan["split"][1] == 0 and plan["split"][5] == 1
+
+
+def test_split_int64():
+    t, D, c = T(1), 18, 2
+    keys = buckets([c * 3 * t + b for b in range(10)], D, 41, dtype=np.int64)
+    keys[::97] = np.iinfo(np.int64).max    # clamped into bucket 9's last sub-range
+    keys[1::89] = np.iinfo(np.int64).min   # clamped into bucket 0's first sub-range
+    plan = check(keys, D, c)
+    assert sum(plan["split"]) >= 8
+
+
+def test_split_pairs_stable():
+    """hs_sort_pairs items (key << 32 | index) go through the split with shift 32: still stable."""
+    t64, c = T(1), 4
+    keys = buckets([c * 3 * t64] * 10, 6, 51)
+    keys[::3] = 345_678                                   # many ties
+    tags = np.random.default_rng(52).integers(0, 2**62, size=keys.size, dtype=np.int64).astype(np.uint64)
+    dk = torch.from_numpy(keys).to(DEV)
+    dt = torch.from_numpy(tags.view(np.int64)).to(DEV)
+    hs.hs_sort_pairs(dk, dt, 6, c)
+    torch.cuda.synchronize()
+    rk, rt = O.sort_pairs(keys, tags, 6, c)
+    assert np.array_equal(dk.cpu().numpy(), rk)
+    assert np.array_equal(dt.cpu().numpy().view(np.uint64), rt)
+
+
+def test_sort_plan_leaves_keys_and_matches_nonsplit_levels():
+    t = T(0)
+    keys = buckets([2 * 3 * t] * 10, 9, 61)
+    d = torch.from_numpy(keys).to(DEV)
+    plan = hs.hs_sort_plan(d, 9, 2)
+    assert np.array_equal(d.cpu().numpy(), keys)          # inspection does not modify keys
+    off = np.concatenate([[0], np.cumsum([2 * 3 * t] * 10)]).astype(np.int64)
+    L_host, k_host = hs.plan_levels(off, 0, 2, 0)
+    for b in range(10):
+        if plan["split"][b]:
+            assert plan["levels"][b] == 1
+        else:
+            assert plan["levels"][b] == L_host[b] and plan["leaves"][b] == 1 << k_host[b]
+    empty = hs.hs_sort_plan(torch.empty(0, dtype=torch.int32, device=DEV), 9, 2)
+    assert empty["split"] == [0] * 10 and empty["levels"] == [0] * 10
