@@ -167,29 +167,49 @@ __global__ void __launch_bounds__(NT, MINB) k_split_pass(const Ctl *__restrict__
     uint32_t *const gb = hist + nsb_cap;                              // SCAT: [nsb_cap] span starts
     K *const skeys = reinterpret_cast<K *>(smem_raw + (((size_t)2 * nsb_cap * 4 + 15) & ~(size_t)15));
     uint32_t *const sdst = reinterpret_cast<uint32_t *>(skeys + TS);
-    const Plan &P = ctl->plan;
-    const SplitCfg &C = ctl->split;
     const int tid = threadIdx.x;
-
-    const long long g = blockIdx.x;
-    if (g >= C.slice_prefix[10]) return;
-    int b = 0;
-    while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
-    if (SCAT && !P.split[b]) return;  // bucket fell back to the merge plan: its keys stay in S
-    const long long r = g - C.slice_prefix[b];
-    const int spc = C.spc[b];
-    const long long j = r / spc, s = r - j * spc;
-    const long long m = P.off[b + 1] - P.off[b];
-    const long long c0 = part_start(m, P.log2c, j), c1 = part_start(m, P.log2c, j + 1);
-    const long long a0 = s * TS;
-    if (a0 >= c1 - c0) return;
-    const int cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
-    const long long cs = P.off[b] + c0;  // chunk start (absolute)
-    const K *in = S + cs + a0;
-    const int ns = P.nsb[b];
-    const long long lo = C.lo[b];
-    const unsigned long long mul = C.mul[b];
-    const int shift = C.shift;
+    // slice geometry: computed once (64-bit divisions) and broadcast
+    struct Desc {
+        long long cs, row, lo;
+        unsigned long long mul;
+        int cnt, ns, shift, a0;
+    };
+    __shared__ Desc sd;
+    if (tid == 0) {
+        const Plan &P = ctl->plan;
+        const SplitCfg &C = ctl->split;
+        const long long g = blockIdx.x;
+        sd.cnt = 0;
+        if (g < C.slice_prefix[10]) {
+            int b = 0;
+            while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
+            if (!SCAT || P.split[b]) {  // a bucket that fell back keeps its keys in S
+                const long long r = g - C.slice_prefix[b];
+                const int spc = C.spc[b];
+                const long long j = r / spc, s = r - j * spc;
+                const long long m = P.off[b + 1] - P.off[b];
+                const long long c0 = part_start(m, P.log2c, j), c1 = part_start(m, P.log2c, j + 1);
+                const long long a0 = s * TS;
+                if (a0 < c1 - c0) {
+                    sd.cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
+                    sd.cs = P.off[b] + c0;  // chunk start (absolute)
+                    sd.a0 = (int)a0;
+                    sd.ns = P.nsb[b];
+                    sd.row = P.sboff[b] + j * (P.nsb[b] + 1);
+                    sd.lo = C.lo[b];
+                    sd.mul = C.mul[b];
+                    sd.shift = C.shift;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int cnt = sd.cnt;
+    if (cnt == 0) return;
+    const long long cs = sd.cs, row = sd.row, lo = sd.lo;
+    const unsigned long long mul = sd.mul;
+    const int ns = sd.ns, shift = sd.shift;
+    const K *in = S + cs + sd.a0;
     HS_DASSERT(ns >= 2 && ns <= nsb_cap);
 
     for (int q = tid; q < ns; q += NT) hist[q] = 0;
@@ -210,7 +230,6 @@ __global__ void __launch_bounds__(NT, MINB) k_split_pass(const Ctl *__restrict__
         }
     }
     __syncthreads();
-    const long long row = P.sboff[b] + j * (ns + 1);
     if constexpr (!SCAT) {
         for (int q = tid; q < ns; q += NT) {
             const uint32_t h = hist[q];

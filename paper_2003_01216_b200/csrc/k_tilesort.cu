@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     int len;
     if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (already in F)
         const int ns = P.nsb[b];
-        const long long j = i / ns, t = i - j * ns;
+        const long long j = (unsigned)i / (unsigned)ns, t = i - j * ns;  // i < c * ns < 2^31
         const uint32_t *e = sbtab + P.sboff[b] + j * (ns + 1) + t;
         lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
         len = (int)(__ldg(e + 1) - __ldg(e));
