@@ -83,6 +83,7 @@ template <typename K>
 __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
                                   const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds) {
     constexpr long long Q = kSampleQ;
+    if (level >= __ldg(&plan_g->Lmax)) return;  // no bucket runs this level (the host only knows a bound)
     __shared__ Plan P;
     load_plan_m(P, plan_g);
     __syncthreads();
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     const int tid = threadIdx.x;
     const K kMax = KeyTraits<K>::kMax;
 
+    if (level >= __ldg(&plan_g->Lmax)) return;  // whole CTA: nothing at this level
     load_plan_m(P, plan_g);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {

@@ -14,16 +14,17 @@
 //
 //   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
 //                    offsets; zeroes the count table
-//   k_split_pass<0>  count: every CTA reads one slice (<= NT*VT keys) of one
-//                    chunk from S, counts its sub-ranges in shared memory and
-//                    adds the non-zero counts to the chunk's table row
+//   k_split_count    persistent CTAs read slices (<= NT*VT keys of one chunk)
+//                    of S, count their sub-ranges in shared memory and add the
+//                    non-zero counts to the chunk's table row (next slice's
+//                    loads in flight during the flush)
 //   k_split_plan     one CTA per chunk: exclusive scan of the row -> sub-range
 //                    starts (+ cursor copy); a sub-range over T keys marks the
 //                    bucket "bad"; the last CTA finalises the Plan: split
 //                    buckets get k = 0, L = log2 c, leaves = sub-ranges; bad
 //                    buckets keep the tile + in-chunk merge plan (skewed keys,
 //                    heavy duplicates: correct either way, only slower)
-//   k_split_pass<1>  scatter: the slice is counted again, every non-empty
+//   k_split_scatter  one CTA per slice: counted again, every non-empty
 //                    sub-range claims its output span with one global atomic,
 //                    the keys are staged by sub-range in shared memory and
 //                    written out run by run (coalesced within a sub-range)
@@ -48,11 +49,11 @@ template <typename K>
 struct SplGeo;
 template <>
 struct SplGeo<int32_t> {
-    static constexpr int NT = 512, VT = 16, MINB_COUNT = 4, MINB_SCAT = 2;
+    static constexpr int NT = 512, VT = 16, MINB_COUNT = 3, MINB_SCAT = 2;
 };
 template <>
 struct SplGeo<int64_t> {
-    static constexpr int NT = 512, VT = 8, MINB_COUNT = 4, MINB_SCAT = 2;
+    static constexpr int NT = 512, VT = 8, MINB_COUNT = 3, MINB_SCAT = 2;
 };
 constexpr int kSplitMaxSub = 4096;  // sub-ranges per chunk (shared-memory counters)
 constexpr int kSplitPlanNT = 512;
@@ -107,14 +108,12 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
 // of bucket b >= 1 has x >= b 10^(D-1) = lo and bucket 0 has lo = 0, so
 // x - lo never overflows.
 __device__ __forceinline__ int sub_range_of(int32_t k, int, long long lo, unsigned long long mul, int ns) {
-    const int32_t d = k - (int32_t)lo;
-    const int t = d < 0 ? 0 : (int)__umulhi((uint32_t)d, (uint32_t)mul);
-    return t < ns ? t : ns - 1;
+    const int32_t d = max(k - (int32_t)lo, 0);
+    return min((int)__umulhi((uint32_t)d, (uint32_t)mul), ns - 1);
 }
 __device__ __forceinline__ int sub_range_of(int64_t k, int shift, long long lo, unsigned long long mul, int ns) {
-    const long long d = (k >> shift) - lo;  // arithmetic shift: the sign of the key survives
-    const long long t = d < 0 ? 0 : (long long)__umul64hi((unsigned long long)d, mul);
-    return t < ns ? (int)t : ns - 1;
+    const long long d = max((k >> shift) - lo, 0LL);  // arithmetic shift: the sign of the key survives
+    return (int)min((long long)__umul64hi((unsigned long long)d, mul), (long long)(ns - 1));
 }
 
 // In-place exclusive scan of a[0, n) by the whole CTA (NT threads, contiguous
@@ -145,125 +144,185 @@ __device__ __forceinline__ void cta_excl_scan(uint32_t *a, int n, uint32_t *wsum
 }
 
 // ------------------------------------------------------------- count / scatter
-// One CTA = one slice of <= NT*VT keys of one chunk.  All VT loads are issued
-// before any use (memory-level parallelism); the shared-memory histogram
-// gives every key its rank among the slice's keys of its sub-range.
-//   count:   the non-zero histogram entries are added to the chunk's row.
-//   scatter: one global atomic per non-empty sub-range claims the slice's
-//            span (issued before the local scan, so its latency overlaps
-//            it); keys are staged at their slice-local sorted position with
-//            their destination, then written in staged order -- consecutive
-//            threads write consecutive addresses within a sub-range.
-template <typename K, int NT, int VT, int MINB, bool SCAT>
-__global__ void __launch_bounds__(NT, MINB) k_split_pass(const Ctl *__restrict__ ctl, const K *__restrict__ S,
-                                                         K *__restrict__ F, uint32_t *tab, uint32_t *cur,
-                                                         int nsb_cap) {
+// A slice = <= TS consecutive keys of one chunk (its slices are numbered
+// bucket by bucket, chunk by chunk).  Its geometry needs 64-bit divisions, so
+// one thread computes it and the CTA reads it from shared memory.
+struct SliceDesc {
+    long long cs, row, lo;  // chunk start (absolute), split-table row, bucket value base
+    unsigned long long mul;
+    int cnt, ns, shift, a0;  // keys in the slice (0: nothing to do), sub-ranges, item shift, offset in chunk
+};
+
+// Called by one thread (the fields share a few cache lines, so after the
+// first miss the chain of loads hits L1).
+__device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long long g, bool need_split, int TS) {
+    const Plan &P = ctl->plan;
+    const SplitCfg &C = ctl->split;
+    sd.cnt = 0;
+    if (g >= C.slice_prefix[10]) return;
+    int b = 0;
+    while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
+    if (need_split && !P.split[b]) return;  // a bucket that fell back keeps its keys in S
+    const unsigned r = (unsigned)(g - C.slice_prefix[b]), spc = (unsigned)C.spc[b];  // < 2^31
+    const long long j = r / spc, s = r - (unsigned)j * spc;
+    const long long m = P.off[b + 1] - P.off[b];
+    const long long c0 = part_start(m, P.log2c, j), c1 = part_start(m, P.log2c, j + 1);
+    const long long a0 = s * TS;
+    if (a0 >= c1 - c0) return;
+    sd.cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
+    sd.cs = P.off[b] + c0;
+    sd.a0 = (int)a0;
+    sd.ns = P.nsb[b];
+    sd.row = P.sboff[b] + j * (P.nsb[b] + 1);
+    sd.lo = C.lo[b];
+    sd.mul = C.mul[b];
+    sd.shift = C.shift;
+}
+
+// Count: persistent CTAs walk the slices with stride gridDim.x.  While the
+// shared histogram of slice g is flushed to its chunk's row (and re-zeroed by
+// the same threads), the keys of the CTA's next slice are already loading.
+// hist[ns] is a dummy sub-range for slots past a slice's end (branch-free).
+template <typename K, int NT, int VT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict__ ctl, const K *__restrict__ S,
+                                                          uint32_t *tab, int nsb_cap) {
     constexpr int TS = NT * VT;
-    constexpr int QMAX = (kSplitMaxSub + NT - 1) / NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
+    __shared__ SliceDesc sd[2];
+    const int tid = threadIdx.x;
+    for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
+    long long g = blockIdx.x;
+    if (tid == 0) slice_desc(sd[0], ctl, g, false, TS);
+    __syncthreads();
+    int cur = 0;
+    K v[VT];
+    {
+        const K *in = S + sd[0].cs + sd[0].a0;
+        const int cnt = sd[0].cnt;
+#pragma unroll
+        for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
+    }
+    const long long nslices = ctl->split.slice_prefix[10];
+    for (; g < nslices; g += gridDim.x) {
+        const SliceDesc &d = sd[cur];
+        if (tid == 0) slice_desc(sd[cur ^ 1], ctl, g + gridDim.x, false, TS);
+        const int cnt = d.cnt, ns = d.ns;
+        if (cnt > 0) {
+            HS_DASSERT(ns >= 2 && ns <= nsb_cap);
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                const int t = k * NT + tid < cnt ? sub_range_of(v[k], d.shift, d.lo, d.mul, ns) : ns;
+                atomicAdd(&hist[t], 1u);
+            }
+        }
+        __syncthreads();  // histogram complete; next descriptor visible
+        const SliceDesc &dn = sd[cur ^ 1];
+        {
+            const K *in = S + dn.cs + dn.a0;
+            const int cn = dn.cnt;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cn ? in[k * NT + tid] : K(0);
+        }
+        if (cnt > 0) {
+            for (int q = tid; q <= ns; q += NT) {
+                const uint32_t h = hist[q];
+                if (h && q < ns) atomicAdd(&tab[d.row + q], h);
+                hist[q] = 0;
+            }
+        }
+        __syncthreads();  // histogram zero again; sd[cur] may be overwritten
+        cur ^= 1;
+    }
+}
+
+// Scatter: one CTA per slice.  Ranks by shared atomics (the dummy sub-range
+// ns takes the slots past the slice's end), one global atomic per non-empty
+// sub-range claims the slice's span (in flight during the local scan), keys
+// are staged at their slice-local sorted position together with their
+// destination (one 64-bit word for int32 keys), then written in staged order:
+// consecutive threads write consecutive addresses inside a sub-range.
+template <typename K, int NT, int VT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
+                                                            K *__restrict__ F, uint32_t *cur, int nsb_cap) {
+    constexpr int TS = NT * VT;
+    constexpr bool PACK = sizeof(K) == 4;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wsum[NT / 32];
-    uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap]
-    uint32_t *const gb = hist + nsb_cap;                              // SCAT: [nsb_cap] span starts
-    K *const skeys = reinterpret_cast<K *>(smem_raw + (((size_t)2 * nsb_cap * 4 + 15) & ~(size_t)15));
+    __shared__ SliceDesc sd;
+    uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
+    unsigned long long *const comb = reinterpret_cast<unsigned long long *>(
+        smem_raw + (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15));  // [nsb_cap + 1]: span << 32 | local start
+    unsigned char *const stage = reinterpret_cast<unsigned char *>(comb + nsb_cap + 1);
+    unsigned long long *const spk = reinterpret_cast<unsigned long long *>(stage);  // PACK: dst << 32 | key
+    K *const skeys = reinterpret_cast<K *>(stage);                                 // !PACK
     uint32_t *const sdst = reinterpret_cast<uint32_t *>(skeys + TS);
     const int tid = threadIdx.x;
-    // slice geometry: computed once (64-bit divisions) and broadcast
-    struct Desc {
-        long long cs, row, lo;
-        unsigned long long mul;
-        int cnt, ns, shift, a0;
-    };
-    __shared__ Desc sd;
-    if (tid == 0) {
-        const Plan &P = ctl->plan;
-        const SplitCfg &C = ctl->split;
-        const long long g = blockIdx.x;
-        sd.cnt = 0;
-        if (g < C.slice_prefix[10]) {
-            int b = 0;
-            while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
-            if (!SCAT || P.split[b]) {  // a bucket that fell back keeps its keys in S
-                const long long r = g - C.slice_prefix[b];
-                const int spc = C.spc[b];
-                const long long j = r / spc, s = r - j * spc;
-                const long long m = P.off[b + 1] - P.off[b];
-                const long long c0 = part_start(m, P.log2c, j), c1 = part_start(m, P.log2c, j + 1);
-                const long long a0 = s * TS;
-                if (a0 < c1 - c0) {
-                    sd.cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
-                    sd.cs = P.off[b] + c0;  // chunk start (absolute)
-                    sd.a0 = (int)a0;
-                    sd.ns = P.nsb[b];
-                    sd.row = P.sboff[b] + j * (P.nsb[b] + 1);
-                    sd.lo = C.lo[b];
-                    sd.mul = C.mul[b];
-                    sd.shift = C.shift;
-                }
-            }
-        }
-    }
+    if (tid == 0) slice_desc(sd, ctl, blockIdx.x, true, TS);
     __syncthreads();
     const int cnt = sd.cnt;
     if (cnt == 0) return;
-    const long long cs = sd.cs, row = sd.row, lo = sd.lo;
-    const unsigned long long mul = sd.mul;
-    const int ns = sd.ns, shift = sd.shift;
+    const long long cs = sd.cs, row = sd.row;
+    const int ns = sd.ns;
     const K *in = S + cs + sd.a0;
     HS_DASSERT(ns >= 2 && ns <= nsb_cap);
 
-    for (int q = tid; q < ns; q += NT) hist[q] = 0;
+    for (int q = tid; q <= ns; q += NT) hist[q] = 0;
     K v[VT];
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int idx = k * NT + tid;
-        v[k] = idx < cnt ? in[idx] : K(0);
-    }
+    for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
     __syncthreads();
     uint32_t tr[VT];  // sub-range << 16 | rank within the slice's keys of that sub-range
+    {
+        const long long lo = sd.lo;
+        const unsigned long long mul = sd.mul;
+        const int shift = sd.shift;
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        if (k * NT + tid < cnt) {
-            const int t = sub_range_of(v[k], shift, lo, mul, ns);
-            if constexpr (SCAT) tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
-            else atomicAdd(&hist[t], 1u);
+        for (int k = 0; k < VT; ++k) {
+            const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
+            tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
         }
     }
     __syncthreads();
-    if constexpr (!SCAT) {
-        for (int q = tid; q < ns; q += NT) {
-            const uint32_t h = hist[q];
-            if (h) atomicAdd(&tab[row + q], h);
-        }
-    } else {
-        uint32_t span[QMAX];
+    // chunk-relative start of this slice's span of sub-range q; the first NT stay in a
+    // register while the scan runs (ns > NT is rare: chunks of > 0.9 T NT keys)
+    uint32_t span0 = 0;
+    if (tid < ns) {
+        const uint32_t h = hist[tid];
+        span0 = h ? atomicAdd(&cur[row + tid], h) : 0u;
+    }
+    for (int q = tid + NT; q < ns; q += NT) {
+        const uint32_t h = hist[q];
+        comb[q] = h ? atomicAdd(&cur[row + q], h) : 0u;
+    }
+    cta_excl_scan<NT>(hist, ns + 1, wsum);  // hist -> slice-local starts (overlaps the atomics)
+    for (int q = tid; q <= ns; q += NT) {
+        const unsigned long long sp = q == tid ? span0 : (q < ns ? comb[q] : 0ull);
+        comb[q] = (sp << 32) | hist[q];
+    }
+    __syncthreads();
 #pragma unroll
-        for (int i = 0; i < QMAX; ++i) {
-            const int q = tid + i * NT;
-            if (q < ns) {
-                const uint32_t h = hist[q];
-                span[i] = h ? atomicAdd(&cur[row + q], h) : 0u;  // chunk-relative start of this slice's span
-            }
+    for (int k = 0; k < VT; ++k) {  // dummy slots land in [cnt, TS) and are not written out
+        const unsigned long long cb = comb[tr[k] >> 16];
+        const uint32_t rk = tr[k] & 0xFFFFu;
+        const uint32_t p = (uint32_t)cb + rk, dst = (uint32_t)(cb >> 32) + rk;
+        if constexpr (PACK) {
+            spk[p] = ((unsigned long long)dst << 32) | (uint32_t)v[k];
+        } else {
+            skeys[p] = v[k];
+            sdst[p] = dst;
         }
-        cta_excl_scan<NT>(hist, ns, wsum);  // hist -> slice-local starts (overlaps the atomics)
-#pragma unroll
-        for (int i = 0; i < QMAX; ++i) {
-            const int q = tid + i * NT;
-            if (q < ns) gb[q] = span[i];
+    }
+    __syncthreads();
+    K *const oc = F + cs;
+    for (int p = tid; p < cnt; p += NT) {
+        if constexpr (PACK) {
+            const unsigned long long w = spk[p];
+            oc[(uint32_t)(w >> 32)] = (K)(uint32_t)w;
+        } else {
+            oc[sdst[p]] = skeys[p];
         }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            if (k * NT + tid < cnt) {
-                const uint32_t t = tr[k] >> 16, rk = tr[k] & 0xFFFFu;
-                const uint32_t p = hist[t] + rk;
-                skeys[p] = v[k];
-                sdst[p] = gb[t] + rk;
-            }
-        }
-        __syncthreads();
-        K *const oc = F + cs;
-        for (int p = tid; p < cnt; p += NT) oc[sdst[p]] = skeys[p];
     }
 }
 
@@ -338,15 +397,19 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
     const int nsb_cap = nsb_bound(n, log2c, tile_keys);
-    const size_t sm_count = (size_t)nsb_cap * 4;
-    const size_t sm_scat = (((size_t)2 * nsb_cap * 4 + 15) & ~(size_t)15) + (size_t)TS * (sizeof(K) + 4);
-    auto kc = k_split_pass<K, G::NT, G::VT, G::MINB_COUNT, false>;
-    auto ks = k_split_pass<K, G::NT, G::VT, G::MINB_SCAT, true>;
+    const size_t sm_count = (size_t)(nsb_cap + 1) * 4;
+    const size_t sm_scat = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 +
+                           (size_t)TS * (sizeof(K) + 4);
+    auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT>;
+    auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat)) != cudaSuccess)
         return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long c = 1LL << log2c;
     const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
     prof_begin(kProfPlan, st);
@@ -354,13 +417,14 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
                                       tab);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
-    kc<<<(unsigned)grid, G::NT, sm_count, st>>>(ctl, S, F, tab, cur, nsb_cap);
+    const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
+    kc<<<(unsigned)pgrid, G::NT, sm_count, st>>>(ctl, S, tab, nsb_cap);
     prof_end(kProfSplitCount, st);
     prof_begin(kProfPlan, st);
     k_split_plan<<<(unsigned)(10 * c), kSplitPlanNT, 0, st>>>(ctl, tab, cur, tile_keys);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
-    ks<<<(unsigned)grid, G::NT, sm_scat, st>>>(ctl, S, F, tab, cur, nsb_cap);
+    ks<<<(unsigned)grid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap);
     prof_end(kProfSplitScatter, st);
     *launches += 4;
     return cudaGetLastError();
