@@ -133,8 +133,8 @@ __device__ __forceinline__ void cta_excl_scan(uint32_t *a, int n, uint32_t *wsum
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    uint32_t base = incl - sum;
-    for (int w = 0; w < warp; ++w) base += wsum[w];
+    const uint32_t wl = lane < NT / 32 && lane < warp ? wsum[lane] : 0u;
+    uint32_t base = incl - sum + __reduce_add_sync(0xffffffffu, wl);  // + totals of the warps before mine
     for (int q = b0; q < b1; ++q) {
         const uint32_t t = a[q];
         a[q] = base;
@@ -236,12 +236,14 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
     }
 }
 
-// Scatter: one CTA per slice.  Ranks by shared atomics (the dummy sub-range
-// ns takes the slots past the slice's end), one global atomic per non-empty
-// sub-range claims the slice's span (in flight during the local scan), keys
-// are staged at their slice-local sorted position together with their
-// destination (one 64-bit word for int32 keys), then written in staged order:
-// consecutive threads write consecutive addresses inside a sub-range.
+// Scatter: persistent CTAs walk the slices with stride gridDim.x (the next
+// slice's descriptor is computed during this one, its keys load during this
+// one's write-out).  Ranks by shared atomics (the dummy sub-range ns takes the
+// slots past the slice's end), one global atomic per non-empty sub-range
+// claims the slice's span (in flight during the local scan), keys are staged
+// at their slice-local sorted position together with their destination (one
+// 64-bit word for int32 keys), then written in staged order: consecutive
+// threads write consecutive addresses inside a sub-range.
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                             K *__restrict__ F, uint32_t *cur, int nsb_cap) {
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wsum[NT / 32];
-    __shared__ SliceDesc sd;
+    __shared__ SliceDesc sd[2];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
     unsigned long long *const comb = reinterpret_cast<unsigned long long *>(
         smem_raw + (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15));  // [nsb_cap + 1]: span << 32 | local start
@@ -259,70 +261,95 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     K *const skeys = reinterpret_cast<K *>(stage);                                 // !PACK
     uint32_t *const sdst = reinterpret_cast<uint32_t *>(skeys + TS);
     const int tid = threadIdx.x;
-    if (tid == 0) slice_desc(sd, ctl, blockIdx.x, true, TS);
+    for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
+    long long g = blockIdx.x;
+    if (tid == 0) slice_desc(sd[0], ctl, g, true, TS);
     __syncthreads();
-    const int cnt = sd.cnt;
-    if (cnt == 0) return;
-    const long long cs = sd.cs, row = sd.row;
-    const int ns = sd.ns;
-    const K *in = S + cs + sd.a0;
-    HS_DASSERT(ns >= 2 && ns <= nsb_cap);
-
-    for (int q = tid; q <= ns; q += NT) hist[q] = 0;
     K v[VT];
-#pragma unroll
-    for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
-    __syncthreads();
-    uint32_t tr[VT];  // sub-range << 16 | rank within the slice's keys of that sub-range
     {
-        const long long lo = sd.lo;
-        const unsigned long long mul = sd.mul;
-        const int shift = sd.shift;
+        const K *in = S + sd[0].cs + sd[0].a0;
+        const int cnt = sd[0].cnt;
 #pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
-            tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
-        }
+        for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
     }
-    __syncthreads();
-    // chunk-relative start of this slice's span of sub-range q; the first NT stay in a
-    // register while the scan runs (ns > NT is rare: chunks of > 0.9 T NT keys)
-    uint32_t span0 = 0;
-    if (tid < ns) {
-        const uint32_t h = hist[tid];
-        span0 = h ? atomicAdd(&cur[row + tid], h) : 0u;
-    }
-    for (int q = tid + NT; q < ns; q += NT) {
-        const uint32_t h = hist[q];
-        comb[q] = h ? atomicAdd(&cur[row + q], h) : 0u;
-    }
-    cta_excl_scan<NT>(hist, ns + 1, wsum);  // hist -> slice-local starts (overlaps the atomics)
-    for (int q = tid; q <= ns; q += NT) {
-        const unsigned long long sp = q == tid ? span0 : (q < ns ? comb[q] : 0ull);
-        comb[q] = (sp << 32) | hist[q];
-    }
-    __syncthreads();
+    const long long nslices = ctl->split.slice_prefix[10];
+    int cb = 0;
+    for (; g < nslices; g += gridDim.x, cb ^= 1) {
+        const SliceDesc &d = sd[cb];
+        if (tid == 0) slice_desc(sd[cb ^ 1], ctl, g + gridDim.x, true, TS);
+        const int cnt = d.cnt, ns = d.ns;
+        if (cnt == 0) {  // nothing here (fallback bucket / past the chunk's end): load the next slice
+            __syncthreads();
+            const SliceDesc &dn = sd[cb ^ 1];
+            const K *in = S + dn.cs + dn.a0;
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {  // dummy slots land in [cnt, TS) and are not written out
-        const unsigned long long cb = comb[tr[k] >> 16];
-        const uint32_t rk = tr[k] & 0xFFFFu;
-        const uint32_t p = (uint32_t)cb + rk, dst = (uint32_t)(cb >> 32) + rk;
-        if constexpr (PACK) {
-            spk[p] = ((unsigned long long)dst << 32) | (uint32_t)v[k];
-        } else {
-            skeys[p] = v[k];
-            sdst[p] = dst;
+            for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < dn.cnt ? in[k * NT + tid] : K(0);
+            __syncthreads();
+            continue;
         }
-    }
-    __syncthreads();
-    K *const oc = F + cs;
-    for (int p = tid; p < cnt; p += NT) {
-        if constexpr (PACK) {
-            const unsigned long long w = spk[p];
-            oc[(uint32_t)(w >> 32)] = (K)(uint32_t)w;
-        } else {
-            oc[sdst[p]] = skeys[p];
+        HS_DASSERT(ns >= 2 && ns <= nsb_cap);
+        uint32_t tr[VT];  // sub-range << 16 | rank within the slice's keys of that sub-range
+        {
+            const long long lo = d.lo;
+            const unsigned long long mul = d.mul;
+            const int shift = d.shift;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
+                tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+            }
         }
+        __syncthreads();
+        // chunk-relative start of this slice's span of sub-range q; the first NT stay in a
+        // register while the scan runs (ns > NT is rare: chunks of > 0.9 T NT keys)
+        const long long row = d.row;
+        uint32_t span0 = 0;
+        if (tid < ns) {
+            const uint32_t h = hist[tid];
+            span0 = h ? atomicAdd(&cur[row + tid], h) : 0u;
+        }
+        for (int q = tid + NT; q < ns; q += NT) {
+            const uint32_t h = hist[q];
+            comb[q] = h ? atomicAdd(&cur[row + q], h) : 0u;
+        }
+        cta_excl_scan<NT>(hist, ns + 1, wsum);  // hist -> slice-local starts (overlaps the atomics)
+        for (int q = tid; q <= ns; q += NT) {
+            const unsigned long long sp = q == tid ? span0 : (q < ns ? comb[q] : 0ull);
+            comb[q] = (sp << 32) | hist[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {  // dummy slots land in [cnt, TS) and are not written out
+            const unsigned long long c = comb[tr[k] >> 16];
+            const uint32_t rk = tr[k] & 0xFFFFu;
+            const uint32_t p = (uint32_t)c + rk, dst = (uint32_t)(c >> 32) + rk;
+            if constexpr (PACK) {
+                spk[p] = ((unsigned long long)dst << 32) | (uint32_t)v[k];
+            } else {
+                skeys[p] = v[k];
+                sdst[p] = dst;
+            }
+        }
+        __syncthreads();  // staged; hist is free; the next descriptor is visible
+        const SliceDesc &dn = sd[cb ^ 1];
+        {
+            const K *in = S + dn.cs + dn.a0;
+            const int cn = dn.cnt;
+#pragma unroll
+            for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cn ? in[k * NT + tid] : K(0);
+            const int nz = (cn > 0 && dn.ns > ns) ? dn.ns : ns;
+            for (int q = tid; q <= nz; q += NT) hist[q] = 0;
+        }
+        K *const oc = F + d.cs;
+        for (int p = tid; p < cnt; p += NT) {
+            if constexpr (PACK) {
+                const unsigned long long w = spk[p];
+                oc[(uint32_t)(w >> 32)] = (K)(uint32_t)w;
+            } else {
+                oc[sdst[p]] = skeys[p];
+            }
+        }
+        __syncthreads();  // staging buffer and sd[cb] free
     }
 }
 
@@ -424,7 +451,8 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     k_split_plan<<<(unsigned)(10 * c), kSplitPlanNT, 0, st>>>(ctl, tab, cur, tile_keys);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
-    ks<<<(unsigned)grid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap);
+    const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
+    ks<<<(unsigned)sgrid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap);
     prof_end(kProfSplitScatter, st);
     *launches += 4;
     return cudaGetLastError();
