@@ -477,7 +477,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                     "K5a split");
     // a5: leaf-tile sort (S, or keys for split buckets) -> (keys | S) per bucket parity
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
-                                     ws.sbtab),
+                                     ws.sbtab, &ws.ctl->split),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);

@@ -32,8 +32,10 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st);
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
 // sbtab: K5a split table (leaves of split buckets; null when no bucket can be split)
+struct SplitCfg;
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
-                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr);
+                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr,
+                             const SplitCfg *scfg = nullptr);
 
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +

@@ -121,8 +121,10 @@ __device__ __forceinline__ void bulk_s2g_ts(void *dst, const void *src, uint32_t
                  : "memory");
 }
 
-__device__ __forceinline__ float to_float_rz(uint32_t u) { return __uint2float_rz(u); }
-__device__ __forceinline__ float to_float_rz(unsigned long long u) { return __ull2float_rz(u); }
+__device__ __forceinline__ uint32_t mulhi_u(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+__device__ __forceinline__ unsigned long long mulhi_u(unsigned long long a, unsigned long long b) {
+    return __umul64hi(a, b);
+}
 
 template <typename K>
 __device__ __forceinline__ K lds_k(uint32_t a);
@@ -148,7 +150,8 @@ struct TSGeo {
 
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
-                                                        K *samp, const uint32_t *__restrict__ sbtab) {
+                                                        K *samp, const uint32_t *__restrict__ sbtab,
+                                                        const SplitCfg *__restrict__ scfg) {
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
@@ -170,6 +173,14 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     const long long i = g - P.tile_prefix[b];
     long long lo;
     int len;
+    using U = typename KeyTraits<K>::U;
+    // frac: an interior sub-range of a split bucket holds exactly the keys x with
+    // mulhi(x - base, mul) = t, and the low word of (x - base) * mul rises with x
+    // across the sub-range -- its top bits are the bucket (no min/max pass).  Edge
+    // sub-ranges (clamped keys) and narrow ones (< 2^12 values: exact counting) don't.
+    bool frac = false;
+    U f_base = 0, f_mul = 0;
+    int f_sft = 0;
     if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (already in F)
         const int ns = P.nsb[b];
         const long long j = (unsigned)i / (unsigned)ns, t = i - j * ns;  // i < c * ns < 2^31
@@ -177,6 +188,13 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
         len = (int)(__ldg(e + 1) - __ldg(e));
         src = F;
+        const U mul = (U)scfg->mul[b];
+        if (t > 0 && t < ns - 1 && mul <= (U)(~(U)0 >> 12)) {
+            frac = true;
+            f_base = (U)scfg->lo[b];
+            f_mul = mul;
+            f_sft = scfg->shift;
+        }
     } else {
         lo = leaf_start(P, b, i);
         len = (int)(leaf_start(P, b, i + 1) - lo);
@@ -227,48 +245,66 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         __shared__ uint32_t bcnt[PACK ? BUCKETS / 2 : BUCKETS];
         __shared__ K red[2][NT / 32];
         __shared__ uint32_t wsum[NT / 32];
-        using U = typename KeyTraits<K>::U;
         const int lane = tid & 31, warp = tid >> 5;
-        K lmin = kMax, lmax = (K)(-kMax - 1);
+        if (!frac) {
+            K lmin = kMax, lmax = (K)(-kMax - 1);
 #pragma unroll
-        for (int k = 0; k < VT; ++k)
-            if (tid * VT + k < len) {
-                lmin = v[k] < lmin ? v[k] : lmin;
-                lmax = v[k] > lmax ? v[k] : lmax;
+            for (int k = 0; k < VT; ++k)
+                if (tid * VT + k < len) {
+                    lmin = v[k] < lmin ? v[k] : lmin;
+                    lmax = v[k] > lmax ? v[k] : lmax;
+                }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const K x = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
+                lmin = x < lmin ? x : lmin;
+                lmax = c > lmax ? c : lmax;
             }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-            const K x = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
-            lmin = x < lmin ? x : lmin;
-            lmax = c > lmax ? c : lmax;
-        }
-        if (lane == 0) {
-            red[0][warp] = lmin;
-            red[1][warp] = lmax;
+            if (lane == 0) {
+                red[0][warp] = lmin;
+                red[1][warp] = lmax;
+            }
         }
 #pragma unroll
         for (int j = 0; j < (PACK ? BPT / 2 : BPT); ++j) bcnt[j * NT + tid] = 0;
         __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
-        K mn = red[0][0], mx = red[1][0];
+        // bucket of k = mulhi(((k >> sft) - base) * mulA, M2): one integer map for all modes
+        //   frac:  base, mulA = the sub-range's (see above), M2 = BUCKETS (top bits of the fraction)
+        //   exact (range < BUCKETS): base = min, mulA = 2^w / BUCKETS, M2 = BUCKETS -> k - min
+        //   else:  base = min, mulA = 1, M2 = floor((2^w - 1) / (range + 1)) BUCKETS (< BUCKETS, monotone)
+        constexpr U WMAX = ~(U)0;
+        U base = f_base, mulA = f_mul, M2 = (U)BUCKETS;
+        int sft = f_sft;
+        bool exact = false, constant = false;
+        K mn = 0;
+        if (!frac) {
+            mn = red[0][0];
+            K mx = red[1][0];
 #pragma unroll
-        for (int w = 1; w < NT / 32; ++w) {
-            mn = red[0][w] < mn ? red[0][w] : mn;
-            mx = red[1][w] > mx ? red[1][w] : mx;
+            for (int w = 1; w < NT / 32; ++w) {
+                mn = red[0][w] < mn ? red[0][w] : mn;
+                mx = red[1][w] > mx ? red[1][w] : mx;
+            }
+            const U range = (U)mx - (U)mn;
+            constant = range == 0;
+            exact = range < (U)BUCKETS;
+            base = (U)mn;
+            sft = 0;
+            if (exact) mulA = (U)(WMAX / (U)BUCKETS + 1);  // 2^w / BUCKETS
+            else {
+                mulA = 1;
+                M2 = range == WMAX ? (U)BUCKETS : WMAX / (range + 1) * (U)BUCKETS;
+            }
         }
-        const U range = (U)mx - (U)mn;
-        if (range == 0) {  // constant tile: every order is the sorted one
+        if (constant) {  // constant tile: every order is the sorted one
             for (int j = tid; j < len; j += NT) so[j] = mn;
             mode = 1;
         } else {
-            // range < BUCKETS: one bucket per key value (an exact counting sort,
-            // buckets need no sort and have no capacity limit)
-            const bool exact = range < (U)BUCKETS;
-            const float scale = (float)BUCKETS / ((float)range + 1.0f);
+            // exact: one bucket per key value (an exact counting sort, buckets need
+            // no sort and have no capacity limit)
             auto bucket_of_key = [&](K k) -> int {
-                const U u = (U)k - (U)mn;
-                if (exact) return (int)u;
-                const int bk = (int)(to_float_rz(u) * scale);  // monotone in k
-                return bk < BUCKETS - 1 ? bk : BUCKETS - 1;
+                const U x = ((U)(k >> sft) - base) * mulA;
+                return (int)mulhi_u(x, M2);  // < BUCKETS, non-decreasing in k
             };
             // returns the bucket's count before this key (its slot when the counters hold starts)
             auto bump = [&](int bk) -> uint32_t {
@@ -477,7 +513,7 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
-                               cudaStream_t st, const uint32_t *sbtab) {
+                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
@@ -491,15 +527,15 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
-    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab);
+    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab, scfg);
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
-                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab);
+                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg);
 }
 
 }  // namespace hs
