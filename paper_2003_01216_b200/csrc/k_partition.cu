@@ -23,6 +23,9 @@
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
+#ifndef HS_K3_SBASE
+#define HS_K3_SBASE 1
+#endif
 #ifndef HS_SCAT_NT
 #define HS_SCAT_NT 128
 #endif
@@ -373,6 +376,13 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
 #pragma unroll
     for (int i = 0; i < 5; ++i)
         base[i] = s_wtot[warp][i] + (w[i] - own[i]) + ((unsigned)s_dstart[2 * i] | ((unsigned)s_dstart[2 * i + 1] << 16));
+#if HS_K3_SBASE
+    // this thread's five packed digit bases in its own shared-memory column (read back
+    // by the thread itself: no barrier; one LDS per key instead of a 4-deep select chain)
+    __shared__ unsigned s_base[5 * NT];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) s_base[i * NT + tid] = base[i];
+#endif
 #pragma unroll
     for (int k0 = 0; k0 < VT; k0 += E) {
         K kv[E];
@@ -384,7 +394,11 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
             const unsigned m = (meta[k >> 2] >> (8 * (k & 3))) & 0xFFu;
             const unsigned d = m & 15u, r = m >> 4;
             if (FULL || d < 10) {
+#if HS_K3_SBASE
+                const unsigned wsel = s_base[(d >> 1) * NT + tid];
+#else
                 const unsigned wsel = d < 2 ? base[0] : d < 4 ? base[1] : d < 6 ? base[2] : d < 8 ? base[3] : base[4];
+#endif
                 const int pos = (int)((wsel >> ((d & 1u) * 16)) & 0xFFFFu) + (int)r;
                 HS_DASSERT(pos >= 0 && pos < T_ && d < 10);
                 sOut[pos] = kv[e];
