@@ -105,11 +105,20 @@ hs_status_t check_inout(const void *in, const void *out, int64_t n, hs_dtype_t d
 }
 
 // 10^(D-1) and the multiply-high magic floor((2^w - 1) / div) (K1).
+// Exact division of a non-negative key u < 2^N (N = w - 1) by div = 10^(D-1):
+// with l = ceil(log2 div) and magic = ceil(2^(N+l) / div) (< 2^w, since
+// 2^(l-1) < div), floor(u / div) = mulhi_w(u, magic) >> (l - 1) for every such
+// u (Granlund & Montgomery 1994, Thm 4.2: 0 <= magic*div - 2^(N+l) < div <= 2^l).
+// The post-shift l - 1 is re-derived from div on the device side (div = 1: q = u).
 void digit_params(int D, hs_dtype_t dt, unsigned long long *div, unsigned long long *magic) {
     unsigned long long d = 1;
     for (int i = 1; i < D; ++i) d *= 10ull;
     *div = d;
-    *magic = dt == HS_INT32 ? (0xFFFFFFFFull / d) : (~0ull / d);
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    const int N = dt == HS_INT32 ? 31 : 63;
+    const unsigned __int128 num = (unsigned __int128)1 << (N + l);
+    *magic = d == 1 ? 0ull : (unsigned long long)((num + d - 1) / d);
 }
 
 // Scratch for one call, one stream-ordered allocation:

@@ -47,32 +47,28 @@ struct KeyTraits<int64_t> {
 
 // Leading decimal digit of a D-digit key, d(k) = clamp(floor(k / 10^(D-1)), 0, 9)
 // (reading #1 zero-padding, #3 clamping).  Division by the runtime
-// constant div = 10^(D-1) is a multiply-high by magic = floor((2^w - 1) / div)
-// plus one correction step: for 0 <= k < 2^(w-1) the estimate is q or q-1
-// (K1), so r = k - est*div lies in [0, 2 div).
+// constant div = 10^(D-1) is exact by one multiply-high and a shift: magic =
+// ceil(2^(N+l) / div), l = ceil(log2 div), N = w - 1, valid for every key in
+// [0, 2^(w-1)) (Granlund-Montgomery, K1); post = l - 1, or -1
+// for div = 1 (the digit is the key itself).
 template <typename K>
 struct DigitParams {
     typename KeyTraits<K>::U div;
     typename KeyTraits<K>::U magic;
     int shift;  // int64 only: the key is k >> shift (32 for the (key << 32 | index) items of hs_sort_pairs)
+    int post;   // post-shift of the multiply-high
 };
 
 __device__ __forceinline__ int msd_digit(int32_t k, const DigitParams<int32_t> &p) {
-    if (k < 0) return 0;
-    uint32_t u = (uint32_t)k;
-    uint32_t q = __umulhi(u, p.magic);
-    uint32_t r = u - q * p.div;
-    q += (r >= p.div) ? 1u : 0u;
+    const uint32_t u = (uint32_t)(k > 0 ? k : 0);  // negative keys clamp to digit 0
+    const uint32_t q = p.post >= 0 ? __umulhi(u, p.magic) >> p.post : u;
     return (int)(q < 9u ? q : 9u);
 }
 
 __device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &p) {
     k >>= p.shift;  // arithmetic: keeps the sign of the key
-    if (k < 0) return 0;
-    unsigned long long u = (unsigned long long)k;
-    unsigned long long q = __umul64hi(u, p.magic);
-    unsigned long long r = u - q * p.div;
-    q += (r >= p.div) ? 1ull : 0ull;
+    const unsigned long long u = (unsigned long long)(k > 0 ? k : 0);
+    const unsigned long long q = p.post >= 0 ? __umul64hi(u, p.magic) >> p.post : u;
     return (int)(q < 9ull ? q : 9ull);
 }
 
@@ -308,6 +304,17 @@ __device__ __forceinline__ void cas(K &a, K &b) {
     K hi = a < b ? b : a;
     a = lo;
     b = hi;
+}
+
+// Two 16-bit keys per register (the tile sort's packed bucket sort): one
+// comparator orders both halves at once (vmin2/vmax2 = one SIMD op each).
+struct H2 {
+    uint32_t v;
+};
+__device__ __forceinline__ void cas(H2 &a, H2 &b) {
+    const uint32_t lo = __vminu2(a.v, b.v), hi = __vmaxu2(a.v, b.v);
+    a.v = lo;
+    b.v = hi;
 }
 
 // Batcher odd-even merge sort network on N registers.  The comparator list

@@ -493,6 +493,11 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     dp.div = (typename KeyTraits<K>::U)div;
     dp.magic = (typename KeyTraits<K>::U)magic;
     dp.shift = key_shift;
+    {
+        int l = 0;
+        while ((1ull << l) < div) ++l;
+        dp.post = div == 1 ? -1 : l - 1;
+    }
     const long long ntiles = ((long long)n + h + TP - 1) / TP;
     if (do_count && ntiles > 0) {
         long long want = (ntiles + kHistWarps - 1) / kHistWarps;
