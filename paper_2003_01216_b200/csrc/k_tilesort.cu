@@ -226,6 +226,9 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
     K *const so = sbuf + sh;  // so[p] <-> out[p]
     int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile / exact counting); 2: buckets to sort
+    // mode 2, int32: every bucket spans < 2^15 values, so a thread's two buckets are
+    // sorted together as 16-bit offsets packed two per register (see below)
+    bool packed = false;
     constexpr int BPT_ = BUCKETS > 0 ? BUCKETS / NT : 1;
     uint32_t bk_base = 0, bk_cnt[BPT_];  // mode 2: my buckets (set before mode becomes 2)
 
@@ -277,6 +280,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         int sft = f_sft;
         bool exact = false, constant = false;
         K mn = 0;
+        // frac: a bucket covers 2^w / (BUCKETS mul) + 1 values -- < 2^15 when mul >= 2^w / 2^24
+        packed = sizeof(K) == 4 && frac && f_mul >= (U)256;
         if (!frac) {
             mn = red[0][0];
             K mx = red[1][0];
@@ -295,6 +300,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 mulA = 1;
                 M2 = range == WMAX ? (U)BUCKETS : WMAX / (range + 1) * (U)BUCKETS;
             }
+            // a bucket spans about (range + 1) / BUCKETS values
+            packed = sizeof(K) == 4 && !exact && range < ((U)1 << 24);
         }
         if (constant) {  // constant tile: every order is the sorted one
             for (int j = tid; j < len; j += NT) so[j] = mn;
@@ -371,7 +378,32 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         }
     }
 
-    if (mode == 2) {
+    if (mode == 2 && packed) {
+        // int32, two buckets per thread, each spanning < 2^15 values: offsets from each
+        // bucket's first key (+2^15, so 0xFFFF pads sort last) packed two per register
+        // -- bucket 0 in the low halves, bucket 1 in the high halves -- and one CAP-key
+        // network of SIMD min/max sorts both buckets at once (half the comparators)
+        __syncthreads();
+        if constexpr (sizeof(K) == 4 && BPT_ == 2) {
+            const uint32_t stA = bk_base, cA = bk_cnt[0], stB = bk_base + bk_cnt[0], cB = bk_cnt[1];
+            if (cA > 1 || cB > 1) {
+                const int32_t rA = cA ? (int32_t)so[stA] : 0, rB = cB ? (int32_t)so[stB] : 0;
+                H2 w[CAP];
+#pragma unroll
+                for (int i = 0; i < CAP; ++i) {
+                    const uint32_t lo = i < (int)cA ? (uint32_t)((int32_t)so[stA + i] - rA + 32768) : 0xFFFFu;
+                    const uint32_t hi = i < (int)cB ? (uint32_t)((int32_t)so[stB + i] - rB + 32768) : 0xFFFFu;
+                    w[i].v = lo | (hi << 16);
+                }
+                oddeven_sort<CAP>(w);
+#pragma unroll
+                for (int i = 0; i < CAP; ++i) {
+                    if (i < (int)cA) so[stA + i] = (K)(rA + (int32_t)(w[i].v & 0xFFFFu) - 32768);
+                    if (i < (int)cB) so[stB + i] = (K)(rB + (int32_t)(w[i].v >> 16) - 32768);
+                }
+            }
+        }
+    } else if (mode == 2) {
         // sort my buckets in registers (v is dead on this path)
         __syncthreads();
         uint32_t st = bk_base;
