@@ -201,9 +201,12 @@ def run_ours(args, cfg):
         tags = torch.empty_like(tags0)
 
     graph = None
-    if args.graph:
-        if shared or pairs:
-            raise SystemExit("--graph applies to hs_sort")
+    if args.graph and (shared or pairs):
+        raise SystemExit("--graph applies to hs_sort")
+    if not (shared or pairs) and not args.no_graph:
+        # the hs_sort call captured once in a CUDA graph (its ~33 launches and the
+        # stream-ordered scratch allocation) and replayed every step: same kernels,
+        # no per-launch host work (default; --no-graph times the direct call)
         graph = hs.SortGraph(buf, cfg.num_digits, cfg.chunks)
 
     def sort_step():
@@ -336,7 +339,7 @@ def run_ours(args, cfg):
             e2e_ms.append(a.elapsed_time(b))
     e2e_serial = statistics.mean(e2e_ms)
     ok_e2e = bool(np.all(h_out.numpy()[1:] >= h_out.numpy()[:-1]))
-    del buf  # the pipeline below holds its own two device slots
+    del buf  # the pipeline below holds its own three device slots
 
     # pipelined stream of batches through the public HostSortPipeline (hs_sort
     # API only): H2D of step i+1 and D2H of step i-1 overlap the sort of step i
@@ -395,7 +398,7 @@ def run_ours(args, cfg):
             "e2e": {"value": world * cfg.n / (e2e * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": e2e,
                     "h2d_bytes_per_step": cfg.n * ksize, "d2h_bytes_per_step": cfg.n * ksize,
                     "how": ("HostSortPipeline (public API): every step copies its batch pinned host -> device, "
-                            "hs_sort, copies the sorted batch device -> pinned host; two device slots and three "
+                            "hs_sort, copies the sorted batch device -> pinned host; three device slots and three "
                             "streams overlap step i+1's H2D and step i-1's D2H with step i's sort; CUDA events "
                             "from the first H2D to the last D2H / K, max over ranks")
                     if e2e_pipe_ms is not None else
@@ -488,7 +491,8 @@ def main():
     ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
     ap.add_argument("--fused", action="store_true", help="with --dist: exchange fused into the scatter kernel")
-    ap.add_argument("--graph", action="store_true", help="replay hs_sort captured in a CUDA graph (small sizes)")
+    ap.add_argument("--graph", action="store_true", help="(default for --api sort) replay hs_sort from a CUDA graph")
+    ap.add_argument("--no-graph", action="store_true", help="time direct hs_sort calls instead of a graph replay")
     args = ap.parse_args()
     import workload as W
     cfg = W.CONFIGS[args.config]

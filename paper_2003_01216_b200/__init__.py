@@ -417,12 +417,15 @@ def hs_sort_host(host_keys, num_digits: int, chunks_per_bucket: int = 8, device=
 class HostSortPipeline:
     """End-to-end sorting of a stream of host batches through hs_sort.
 
-    Each batch goes pinned host -> H2D -> hs_sort -> D2H.  Two device slots
-    and three CUDA streams (H2D copy, compute, D2H copy) let the H2D of batch
-    i+1 and the D2H of batch i-1 run on the copy engines while batch i is
-    sorted, so a long stream of batches is bounded by the slowest of the three
-    stages instead of their sum.  Ordering is kept with CUDA events only (no
-    host synchronisation except when a slot is reused and in ``finish``).
+    Each batch goes pinned host -> H2D -> hs_sort -> D2H.  ``slots`` device
+    buffers (default 3) and three CUDA streams (H2D copy, compute, D2H copy) let
+    the H2D of batch i+1 and the D2H of batch i-1 run on the two copy engines
+    (opposite PCIe directions, concurrently) while batch i is sorted, so a long
+    stream of batches is bounded by the slowest of the three stages instead of
+    their sum.  With 2 slots the H2D of batch i+1 would wait for the D2H of
+    batch i-1 and the copies would serialise; 3 keep both directions busy.
+    Ordering is kept with CUDA events only (no host synchronisation except in
+    ``finish``).
 
         pipe = HostSortPipeline(n, torch.int32, num_digits=9, chunks=8)
         for h_in, h_out in batches:      # pinned CPU tensors of n keys
@@ -430,20 +433,22 @@ class HostSortPipeline:
         pipe.finish()
     """
 
-    def __init__(self, n: int, dtype, num_digits: int, chunks: int = 8, device=None):
+    def __init__(self, n: int, dtype, num_digits: int, chunks: int = 8, device=None, slots: int = 3):
         torch = _torch()
+        if slots < 1:
+            raise ValueError("slots must be >= 1")
         self.dev = torch.device(device or "cuda")
         self.n, self.num_digits, self.chunks = n, num_digits, chunks
-        self.bufs = [torch.empty(n, dtype=dtype, device=self.dev) for _ in range(2)]
+        self.bufs = [torch.empty(n, dtype=dtype, device=self.dev) for _ in range(slots)]
         self.s_in = torch.cuda.Stream(self.dev)
         self.s_cmp = torch.cuda.Stream(self.dev)
         self.s_out = torch.cuda.Stream(self.dev)
-        self.out_done = [None, None]  # event: slot's D2H finished (slot free again)
+        self.out_done = [None] * slots  # event: slot's D2H finished (slot free again)
         self.i = 0
 
     def submit(self, h_in, h_out) -> None:
         torch = _torch()
-        slot = self.i & 1
+        slot = self.i % len(self.bufs)
         buf = self.bufs[slot]
         ev_free = self.out_done[slot]
         with torch.cuda.stream(self.s_in):

@@ -377,13 +377,15 @@ def test_merge_and_chunks_misaligned_views(dtype, shift):
     assert np.all(got[:shift] == 0) and np.all(got[shift + n:] == 0)
 
 
-def test_host_sort_pipeline():
-    """HostSortPipeline (public e2e API): every batch of a stream comes back sorted."""
+@pytest.mark.parametrize("slots", [1, 2, 3])
+def test_host_sort_pipeline(slots):
+    """HostSortPipeline (public e2e API): every batch of a stream comes back sorted, whatever the
+    number of device slots the batches rotate through (slot reuse is ordered by events only)."""
     n = 300_011
     batches = [W.uniform(n, 300 + i, 10**9, dtype=np.int32) for i in range(5)]
     h_in = [torch.from_numpy(b).pin_memory() for b in batches]
     h_out = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in batches]
-    pipe = hs.HostSortPipeline(n, torch.int32, 9, 8, device=DEV)
+    pipe = hs.HostSortPipeline(n, torch.int32, 9, 8, device=DEV, slots=slots)
     for a, b in zip(h_in, h_out):
         pipe.submit(a, b)
     pipe.finish()

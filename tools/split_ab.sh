@@ -1,6 +1,3 @@
-mkdir -p gpurun_out/s13
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s13/tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/s13/tests.log
-for c in C3 C2 C4 P3; do
-  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline >> gpurun_out/s13/b_$c.json 2>> gpurun_out/s13/b_$c.log
-done
-timeout 300 python bench.py --api pairs --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s13/b_pairs.json 2> gpurun_out/s13/b_pairs.log
+mkdir -p gpurun_out/s16
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "pipeline or graph" > gpurun_out/s16/tests.log 2>&1; echo "rc=$?" >> gpurun_out/s16/tests.log
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/s16/b.json 2> gpurun_out/s16/b.log
