@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/e4
-python tools/exp.py run main pk > gpurun_out/e4/exp.log 2>&1
-python tools/exp.py run main pk >> gpurun_out/e4/exp.log 2>&1
+mkdir -p gpurun_out/e5
+python tools/exp.py run main crpf crpf3 > gpurun_out/e5/exp.log 2>&1
+python tools/exp.py run main crpf crpf3 >> gpurun_out/e5/exp.log 2>&1
