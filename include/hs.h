@@ -137,10 +137,11 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
  * each bucket's last merge level writes straight into keys.
  * Sorting a chunk larger than one tile starts with one quicksort-style
  * partition step with many pivots (K5a): the chunk is split by key value into
- * equal-width sub-ranges of its bucket's digit range, each of which is then
- * sorted in one shared-memory tile; a bucket whose sub-ranges overflow a tile
- * (skewed keys, heavy duplicates) falls back to tile sort + in-chunk merge
- * levels.  Either way the result is the unique ascending array.  The split
+ * equal-width sub-ranges of its bucket's digit range (or, for a bucket whose
+ * sampled key distribution is skewed, equal-count groups of 2048 fine bins),
+ * each of which is then sorted in one shared-memory tile; a bucket whose
+ * sub-ranges still overflow a tile (a value with more than a tile of copies in
+ * a chunk) falls back to tile sort + in-chunk merge levels.  Either way the result is the unique ascending array.  The split
  * is on unless the environment variable HS_SPLIT=0 is set (A/B measurements).
  *
  *   keys[n]            in/out: device; ascending on return.

@@ -102,13 +102,20 @@ struct Plan {
     int Lmax;
 };
 
-// K5a bookkeeping (value split of the chunks), written by k_split_setup.
+// K5a bookkeeping (value split of the chunks), written by k_split_setup and
+// k_split_map.  Fine bins: kSplitFine equal-width bins of a bucket's digit
+// range, the unit of the sampled sub-range map of skewed buckets (fine enough
+// that one bin near a C4-like peak holds ~0.06 T keys of a chunk).
+constexpr int kSplitFine = 8192;
 struct SplitCfg {
     long long slice_prefix[11];  // CTAs of the count / scatter passes per bucket (c * spc[b])
     long long lo[10];            // bucket b's value range starts at b * 10^(D-1)
     unsigned long long mul[10];  // sub-range of x = mulhi(x - lo, mul), mul = floor((2^w - 1) / 10^(D-1)) nsb[b]
+    unsigned long long fmul[10]; // fine bin of x = min(mulhi(x - lo, fmul), kSplitFine - 1) (0: no fine bins)
     int spc[10];                 // slices per chunk
     int cand[10];                // bucket b is split if no sub-range of its chunks exceeds T
+    int mode[10];                // 0: equal-width sub-ranges (mul); 1: sub-range = map[b][fine bin] (skewed bucket)
+    int nsa[10];                 // split-table row capacity per chunk - 1 (nsb[b] <= nsa[b])
     unsigned bad;                // buckets with an over-full sub-range (fall back to merge levels)
     unsigned ticket;
     int shift;                   // sort key of an item = item >> shift (hs_sort_pairs)

@@ -14,6 +14,11 @@
 //
 //   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
 //                    offsets; zeroes the count table
+//   k_split_sample   10 x 8 CTAs: fine-bin histograms of a 32k-key sample of
+//                    every candidate bucket
+//   k_split_map      one CTA per bucket: keeps equal-width sub-ranges unless
+//                    the sample's largest count is beyond the sampling noise
+//                    of a uniform bucket, else writes the equal-count map
 //   k_split_count    persistent CTAs read slices (<= NT*VT keys of one chunk)
 //                    of S, count their sub-ranges in shared memory and add the
 //                    non-zero counts to the chunk's table row (next slice's
@@ -32,12 +37,13 @@
 // The order of keys inside a sub-range depends on atomic arrival order; the
 // tile sort that follows makes the result the unique sorted chunk (keys only;
 // hs_sort_pairs sorts unique (key << 32 | index) items, so stays stable).
-// Sub-range of a key: floor((x - lo_b) * nsb / 10^(D-1)) in fp32, clamped to
-// [0, nsb) -- a monotone function of the key (int -> float rounding, scaling
-// by a positive constant and truncation are all monotone), so sub-range order
-// is key order; keys clamped into bucket 0 / 9 (P:78 reading #3) land in the
-// first / last sub-range.  Roofline: HBM, 4 B read (count) + 8 B read+write
-// (scatter) per int32 key.
+// Sub-range of a key: min(mulhi(max(x - lo_b, 0), mul), nsb - 1) with mul =
+// floor((2^w - 1) / 10^(D-1)) nsb -- non-decreasing in the key, so sub-range
+// order is key order; keys clamped into bucket 0 / 9 (P:78 reading #3) land in
+// the first / last sub-range.  Skewed buckets (k_split_sample / k_split_map)
+// use equal-count groups of 8192 fine equal-width bins instead, picked from a
+// 32k-key sample: map[fine bin] is non-decreasing, so the order argument holds.
+// Roofline: HBM, 4 B read (count) + 8 B read+write (scatter) per int32 key.
 #include <cstdint>
 
 #include "hs_device.cuh"
@@ -61,6 +67,10 @@ constexpr int kSplitPlanNT = 512;
 __host__ __device__ __forceinline__ long long split_target(int tile_keys) { return (long long)tile_keys * 9 / 10; }
 
 // ------------------------------------------------------------------ setup
+// Row capacity per chunk for a sampled (skewed) bucket: sub-ranges of ~0.7 T
+// keys (slack for the sampling error of the map).
+__host__ __device__ __forceinline__ long long split_target_map(int tile_keys) { return (long long)tile_keys * 7 / 10; }
+
 __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, int key_shift, int tile_keys,
                               int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab) {
     __shared__ long long s_words;
@@ -68,29 +78,40 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
         Plan &P = ctl->plan;
         SplitCfg &C = ctl->split;
         const long long c = 1LL << P.log2c, target = split_target(tile_keys);
+        const long long target_m = split_target_map(tile_keys);
+        const unsigned long long wmax = key_bits == 32 ? 0xFFFFFFFFull : ~0ull;
         long long acc_s = 0, acc_t = 0;
         for (int b = 0; b < 10; ++b) {
             const long long m = P.off[b + 1] - P.off[b], cm = (m + c - 1) / c;
             const long long ns = (cm + target - 1) / target;
+            long long nsa = (cm + target_m - 1) / target_m;
+            if (nsa > nsb_cap) nsa = nsb_cap;
+            if (nsa < ns) nsa = ns;
             // ns <= div: the multiplier below fits the key width (and narrower sub-ranges would be empty)
             const bool cand = P.k[b] > 0 && ns >= 2 && ns <= nsb_cap && (unsigned long long)ns <= div &&
-                              acc_t + c * (ns + 1) <= tab_cap;
+                              acc_t + c * (nsa + 1) <= tab_cap;
             C.cand[b] = cand;
+            C.mode[b] = 0;
             C.slice_prefix[b] = acc_s;
             if (cand) {
                 const long long spc = (cm + slice_keys - 1) / slice_keys;
                 C.spc[b] = (int)spc;
                 acc_s += c * spc;
                 P.nsb[b] = (int)ns;
+                C.nsa[b] = (int)nsa;
                 P.sboff[b] = acc_t;
-                acc_t += c * (ns + 1);
+                acc_t += c * (nsa + 1);
                 C.lo[b] = (long long)b * (long long)div;
-                const unsigned long long wmax = key_bits == 32 ? 0xFFFFFFFFull : ~0ull;
                 C.mul[b] = wmax / div * (unsigned long long)ns;  // <= wmax since ns <= div
+                // fine bins for the sampled map (needs >= 1 value per fine bin; nsa <= kSplitFine)
+                C.fmul[b] = (div >= (unsigned long long)kSplitFine && nsa <= kSplitFine)
+                                ? wmax / div * (unsigned long long)kSplitFine : 0ull;
             } else {
                 C.spc[b] = 1;
                 C.lo[b] = 0;
                 C.mul[b] = 0;
+                C.fmul[b] = 0;
+                C.nsa[b] = 0;
             }
         }
         C.slice_prefix[10] = acc_s;
@@ -99,6 +120,126 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
     }
     __syncthreads();
     for (long long q = threadIdx.x; q < s_words; q += blockDim.x) tab[q] = 0;
+}
+
+// ------------------------------------------------------------------ sampled map
+// Equal-width sub-ranges fit keys spread over the digit range (C2, C3, C5, P3).
+// For a skewed bucket (C4: a normal peak) k_split_sample histograms a sample of
+// the bucket over kSplitFine fine bins, and k_split_map either keeps the equal-
+// width sub-ranges (their largest sample count is within mean + 5 sqrt(mean))
+// or replaces them by equal-count groups of consecutive fine bins:
+// map[i] = floor(excl_prefix(i) * ns' / total), non-decreasing in i, so the
+// sub-range order is still key order.  The exact count pass decides as before
+// (an over-full sub-range -- e.g. one value with > T copies in a chunk -- makes
+// the bucket fall back).
+constexpr int kSampleCTAs = 8, kSamplePerCTA = 4096;  // 32k samples per candidate bucket
+
+template <typename K>
+__device__ __forceinline__ int fine_bin(K k, int shift, long long lo, unsigned long long fmul);
+template <>
+__device__ __forceinline__ int fine_bin<int32_t>(int32_t k, int, long long lo, unsigned long long fmul) {
+    const int32_t d = max(k - (int32_t)lo, 0);
+    return min((int)__umulhi((uint32_t)d, (uint32_t)fmul), kSplitFine - 1);
+}
+template <>
+__device__ __forceinline__ int fine_bin<int64_t>(int64_t k, int shift, long long lo, unsigned long long fmul) {
+    const long long d = max((k >> shift) - lo, 0LL);
+    return (int)min((long long)__umul64hi((unsigned long long)d, fmul), (long long)(kSplitFine - 1));
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) k_split_sample(const Ctl *__restrict__ ctl, const K *__restrict__ S,
+                                                      uint32_t *fhist) {
+    __shared__ uint32_t h[kSplitFine];
+    const int b = blockIdx.x / kSampleCTAs, part = blockIdx.x % kSampleCTAs;
+    const SplitCfg &C = ctl->split;
+    const Plan &P = ctl->plan;
+    if (!C.cand[b] || C.fmul[b] == 0) return;
+    for (int q = threadIdx.x; q < kSplitFine; q += blockDim.x) h[q] = 0;
+    __syncthreads();
+    const long long m = P.off[b + 1] - P.off[b], base = P.off[b];
+    const long long tot = (long long)kSampleCTAs * kSamplePerCTA;
+    const long long lo = C.lo[b];
+    const unsigned long long fmul = C.fmul[b];
+    const int shift = C.shift;
+    constexpr int PER = kSamplePerCTA / 256;
+    K kk[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {  // all loads in flight first
+        const long long r = (long long)part * kSamplePerCTA + j * 256 + threadIdx.x;  // evenly spaced positions
+        kk[j] = __ldg(S + base + (long long)((unsigned long long)r * (unsigned long long)m / (unsigned long long)tot));
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
+    __syncthreads();
+    uint32_t *const out = fhist + ((size_t)b * kSampleCTAs + part) * kSplitFine;  // this CTA's histogram
+    for (int q = threadIdx.x; q < kSplitFine; q += blockDim.x) out[q] = h[q];
+}
+
+__global__ void __launch_bounds__(1024) k_split_map(Ctl *ctl, const uint32_t *__restrict__ fhist, uint16_t *map,
+                                                    int tile_keys) {
+    constexpr int NT = 1024, PER = kSplitFine / NT;
+    static_assert(kSplitFine % NT == 0, "fine bins per thread");
+    __shared__ uint32_t est[kSplitFine];  // equal-width sub-range estimates (ns <= nsa <= kSplitFine)
+    __shared__ uint32_t wsum[NT / 32];
+    __shared__ unsigned s_max;
+    Plan &P = ctl->plan;
+    SplitCfg &C = ctl->split;
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!C.cand[b] || C.fmul[b] == 0) return;
+    const int ns = P.nsb[b];
+    uint32_t h[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        h[j] = 0;
+        for (int part = 0; part < kSampleCTAs; ++part)  // sum of the sampling CTAs' histograms
+            h[j] += fhist[((size_t)b * kSampleCTAs + part) * kSplitFine + tid * PER + j];
+        sum += h[j];
+    }
+    for (int q = tid; q < ns; q += NT) est[q] = 0;
+    if (tid == 0) s_max = 0;
+    // block exclusive scan of the per-thread sums
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    const uint32_t wl = lane < NT / 32 && lane < warp ? wsum[lane] : 0u;
+    const uint32_t excl0 = incl - sum + __reduce_add_sync(0xffffffffu, wl);
+    const uint32_t wt = lane < NT / 32 ? wsum[lane] : 0u;
+    const uint32_t total = __reduce_add_sync(0xffffffffu, wt);
+    // equal-width estimate: fine bin i lies (about) in sub-range floor(i ns / kSplitFine)
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+        if (h[j]) atomicAdd(&est[(tid * PER + j) * ns / kSplitFine], h[j]);
+    __syncthreads();
+    for (int q = tid; q < ns; q += NT) atomicMax(&s_max, est[q]);
+    __syncthreads();
+    // keep equal width unless the largest sample count is beyond the sampling noise of a
+    // uniform bucket: > mean + 5 sqrt(mean) + 1 (mean = total / ns samples per sub-range;
+    // the max of ns Poisson counts stays within ~3.5 sqrt(mean) of it)
+    const float mean_s = (float)total / (float)ns;
+    const bool skewed = total > 0 && (float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f;
+    if (!skewed) return;  // mode stays 0
+    const long long c = 1LL << P.log2c, m = P.off[b + 1] - P.off[b], cm = (m + c - 1) / c;
+    const long long tm = split_target_map(tile_keys);
+    long long ns2 = (cm + tm - 1) / tm;
+    if (ns2 > C.nsa[b]) ns2 = C.nsa[b];
+    if (ns2 < 2) ns2 = 2;
+    uint32_t run = excl0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const long long g = (long long)run * ns2 / total;
+        map[b * kSplitFine + tid * PER + j] = (uint16_t)(g < ns2 - 1 ? g : ns2 - 1);
+        run += h[j];
+    }
+    if (tid == 0) {
+        P.nsb[b] = (int)ns2;
+        C.mode[b] = 1;
+    }
 }
 
 // ------------------------------------------------------------------ helpers
@@ -149,13 +290,15 @@ __device__ __forceinline__ void cta_excl_scan(uint32_t *a, int n, uint32_t *wsum
 // one thread computes it and the CTA reads it from shared memory.
 struct SliceDesc {
     long long cs, row, lo;  // chunk start (absolute), split-table row, bucket value base
-    unsigned long long mul;
+    unsigned long long mul, fmul;
+    const uint16_t *bmap;    // sampled sub-range map of the bucket (null: equal width)
     int cnt, ns, shift, a0;  // keys in the slice (0: nothing to do), sub-ranges, item shift, offset in chunk
 };
 
 // Called by one thread (the fields share a few cache lines, so after the
 // first miss the chain of loads hits L1).
-__device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long long g, bool need_split, int TS) {
+__device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long long g, bool need_split, int TS,
+                                           const uint16_t *map) {
     const Plan &P = ctl->plan;
     const SplitCfg &C = ctl->split;
     sd.cnt = 0;
@@ -176,6 +319,8 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
     sd.row = P.sboff[b] + j * (P.nsb[b] + 1);
     sd.lo = C.lo[b];
     sd.mul = C.mul[b];
+    sd.fmul = C.fmul[b];
+    sd.bmap = C.mode[b] ? map + b * kSplitFine : nullptr;
     sd.shift = C.shift;
 }
 
@@ -185,7 +330,7 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
 // hist[ns] is a dummy sub-range for slots past a slice's end (branch-free).
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict__ ctl, const K *__restrict__ S,
-                                                          uint32_t *tab, int nsb_cap) {
+                                                          uint32_t *tab, int nsb_cap, const uint16_t *map) {
     constexpr int TS = NT * VT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
@@ -193,7 +338,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
     const int tid = threadIdx.x;
     for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
     long long g = blockIdx.x;
-    if (tid == 0) slice_desc(sd[0], ctl, g, false, TS);
+    if (tid == 0) slice_desc(sd[0], ctl, g, false, TS, map);
     __syncthreads();
     int cur = 0;
     K v[VT];
@@ -206,14 +351,22 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
     const long long nslices = ctl->split.slice_prefix[10];
     for (; g < nslices; g += gridDim.x) {
         const SliceDesc &d = sd[cur];
-        if (tid == 0) slice_desc(sd[cur ^ 1], ctl, g + gridDim.x, false, TS);
+        if (tid == 0) slice_desc(sd[cur ^ 1], ctl, g + gridDim.x, false, TS, map);
         const int cnt = d.cnt, ns = d.ns;
         if (cnt > 0) {
             HS_DASSERT(ns >= 2 && ns <= nsb_cap);
+            if (d.bmap == nullptr) {  // equal width (uniform per slice: the branch is outside the key loop)
+                const long long lo = d.lo;
+                const unsigned long long mul = d.mul;
 #pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                const int t = k * NT + tid < cnt ? sub_range_of(v[k], d.shift, d.lo, d.mul, ns) : ns;
-                atomicAdd(&hist[t], 1u);
+                for (int k = 0; k < VT; ++k)
+                    atomicAdd(&hist[k * NT + tid < cnt ? sub_range_of(v[k], d.shift, lo, mul, ns) : ns], 1u);
+            } else {
+#pragma unroll
+                for (int k = 0; k < VT; ++k)
+                    atomicAdd(&hist[k * NT + tid < cnt ? (int)__ldg(d.bmap + fine_bin<K>(v[k], d.shift, d.lo, d.fmul))
+                                                       : ns],
+                              1u);
             }
         }
         __syncthreads();  // histogram complete; next descriptor visible
@@ -246,7 +399,8 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
 // threads write consecutive addresses inside a sub-range.
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
-                                                            K *__restrict__ F, uint32_t *cur, int nsb_cap) {
+                                                            K *__restrict__ F, uint32_t *cur, int nsb_cap,
+                                                            const uint16_t *map) {
     constexpr int TS = NT * VT;
     constexpr bool PACK = sizeof(K) == 4;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
@@ -263,7 +417,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     const int tid = threadIdx.x;
     for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
     long long g = blockIdx.x;
-    if (tid == 0) slice_desc(sd[0], ctl, g, true, TS);
+    if (tid == 0) slice_desc(sd[0], ctl, g, true, TS, map);
     __syncthreads();
     K v[VT];
     {
@@ -276,7 +430,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     int cb = 0;
     for (; g < nslices; g += gridDim.x, cb ^= 1) {
         const SliceDesc &d = sd[cb];
-        if (tid == 0) slice_desc(sd[cb ^ 1], ctl, g + gridDim.x, true, TS);
+        if (tid == 0) slice_desc(sd[cb ^ 1], ctl, g + gridDim.x, true, TS, map);
         const int cnt = d.cnt, ns = d.ns;
         if (cnt == 0) {  // nothing here (fallback bucket / past the chunk's end): load the next slice
             __syncthreads();
@@ -291,12 +445,21 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
         uint32_t tr[VT];  // sub-range << 16 | rank within the slice's keys of that sub-range
         {
             const long long lo = d.lo;
-            const unsigned long long mul = d.mul;
+            const unsigned long long mul = d.mul, fmul = d.fmul;
+            const uint16_t *const bmap = d.bmap;
             const int shift = d.shift;
+            if (bmap == nullptr) {
 #pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
-                tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
+                    tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NT + tid < cnt ? (int)__ldg(bmap + fine_bin<K>(v[k], shift, lo, fmul)) : ns;
+                    tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+                }
             }
         }
         __syncthreads();
@@ -407,12 +570,15 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
 }
 
 // ------------------------------------------------------------------ host
+// words after the split table: fine histograms (u32) and sampled maps (u16) of the 10 buckets
+constexpr long long kSplitExtraWords = 10LL * kSampleCTAs * kSplitFine + 10LL * kSplitFine / 2;
+
 long long split_table_words(long long n, int log2c, int tile_keys) {
-    return n / split_target(tile_keys) + 40 * (1LL << log2c) + 64;
+    return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + kSplitExtraWords;
 }
 
 static int nsb_bound(long long n, int log2c, int tile_keys) {
-    const long long c = 1LL << log2c, cm = (n + c - 1) / c, t = split_target(tile_keys);
+    const long long c = 1LL << log2c, cm = (n + c - 1) / c, t = split_target_map(tile_keys);
     const long long ns = (cm + t - 1) / t;
     return (int)(ns < kSplitMaxSub ? (ns < 2 ? 2 : ns) : kSplitMaxSub);
 }
@@ -439,22 +605,27 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long c = 1LL << log2c;
     const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
+    const long long tab_cap = tab_words - kSplitExtraWords;
+    uint32_t *const fhist = tab + tab_cap;
+    uint16_t *const map = reinterpret_cast<uint16_t *>(fhist + 10 * kSampleCTAs * kSplitFine);
     prof_begin(kProfPlan, st);
-    k_split_setup<<<1, 1024, 0, st>>>(ctl, div, 8 * (int)sizeof(K), key_shift, tile_keys, TS, tab_words, nsb_cap,
+    k_split_setup<<<1, 1024, 0, st>>>(ctl, div, 8 * (int)sizeof(K), key_shift, tile_keys, TS, tab_cap, nsb_cap,
                                       tab);
+    k_split_sample<K><<<10 * kSampleCTAs, 256, 0, st>>>(ctl, S, fhist);
+    k_split_map<<<10, 1024, 0, st>>>(ctl, fhist, map, tile_keys);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
-    kc<<<(unsigned)pgrid, G::NT, sm_count, st>>>(ctl, S, tab, nsb_cap);
+    kc<<<(unsigned)pgrid, G::NT, sm_count, st>>>(ctl, S, tab, nsb_cap, map);
     prof_end(kProfSplitCount, st);
     prof_begin(kProfPlan, st);
     k_split_plan<<<(unsigned)(10 * c), kSplitPlanNT, 0, st>>>(ctl, tab, cur, tile_keys);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
     const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
-    ks<<<(unsigned)sgrid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap);
+    ks<<<(unsigned)sgrid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap, map);
     prof_end(kProfSplitScatter, st);
-    *launches += 4;
+    *launches += 6;
     return cudaGetLastError();
 }
 

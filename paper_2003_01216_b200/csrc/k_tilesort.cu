@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         len = (int)(__ldg(e + 1) - __ldg(e));
         src = F;
         const U mul = (U)scfg->mul[b];
-        if (t > 0 && t < ns - 1 && mul <= (U)(~(U)0 >> 12)) {
+        if (scfg->mode[b] == 0 && t > 0 && t < ns - 1 && mul <= (U)(~(U)0 >> 12)) {
             frac = true;
             f_base = (U)scfg->lo[b];
             f_mul = mul;

@@ -85,7 +85,8 @@ def test_split_just_over_one_tile():
 
 
 def test_split_mixed_with_fallback_buckets():
-    """Buckets 1, 4, 7 split; 2 (one value), 5 (narrow peak), 9 (clamped keys) fall back; 0, 3 fit a tile."""
+    """Buckets 1, 4, 7 split (equal width), 6 splits through the sampled map (a narrow normal peak);
+    2 (one value), 5 (three values), 9 (clamped keys) fall back; 0, 3 fit a tile."""
     t, D, c = T(0), 7, 2
     div = 10 ** (D - 1)
     rng = np.random.default_rng(3)
@@ -96,15 +97,16 @@ def test_split_mixed_with_fallback_buckets():
         np.full(m, 2 * div + 12345),                           # bucket 2: constant -> over-full sub-range
         rng.integers(3 * div, 4 * div, size=t // 2),           # bucket 3: small
         rng.integers(4 * div, 5 * div, size=m + 999),          # bucket 4: split
-        5 * div + rng.integers(0, 1000, size=m),               # bucket 5: all in the first sub-range
-        rng.integers(7 * div, 8 * div, size=m - 5),            # bucket 7: split (bucket 6 empty)
+        5 * div + rng.integers(0, 3, size=m),                  # bucket 5: three values, > T copies each per chunk
+        np.clip(rng.normal(6.5 * div, div / 40, size=m), 6 * div, 7 * div - 1).astype(np.int64),  # bucket 6: peak
+        rng.integers(7 * div, 8 * div, size=m - 5),            # bucket 7: split
         rng.integers(10 * div, 2**31 - 1, size=m),             # bucket 9: clamped (>= 10^D): last sub-range
     ]
     keys = np.concatenate(parts).astype(np.int32)
     rng.shuffle(keys)
     plan = check(keys, D, c)
-    assert [plan["split"][b] for b in (1, 4, 7)] == [1, 1, 1]
-    assert [plan["split"][b] for b in (0, 2, 3, 5, 6, 9)] == [0] * 6
+    assert [plan["split"][b] for b in (1, 4, 6, 7)] == [1, 1, 1, 1]
+    assert [plan["split"][b] for b in (0, 2, 3, 5, 9)] == [0] * 5
     assert plan["levels"][1] == 1 and plan["levels"][2] > 1    # fallback keeps its in-chunk levels
 
 
@@ -177,3 +179,35 @@ def test_sort_plan_leaves_keys_and_matches_nonsplit_levels():
             assert plan["levels"][b] == L_host[b] and plan["leaves"][b] == 1 << k_host[b]
     empty = hs.hs_sort_plan(torch.empty(0, dtype=torch.int32, device=DEV), 9, 2)
     assert empty["split"] == [0] * 10 and empty["levels"] == [0] * 10
+
+
+def test_split_skewed_mixture_uses_sampled_map():
+    """C4's mixture (70% one normal peak across buckets 2-3, 20% from a 1024-value table, 10% uniform):
+    equal-width sub-ranges of the peak buckets would overflow a tile; the sampled map splits them."""
+    keys = W.generate("C4", 0, 6_000_000)
+    plan = check(keys, 9, 8)
+    assert plan["split"][2] == 1 and plan["split"][3] == 1
+    assert plan["levels"][2] == 3 and plan["levels"][3] == 3
+
+
+def test_split_sampled_map_int64_and_pairs():
+    """The sampled map on int64 keys (a peak in bucket 4) and on hs_sort_pairs items (shift 32)."""
+    rng = np.random.default_rng(71)
+    D, n = 18, 10 * 2 * 4 * T(1)
+    div = 10 ** (D - 1)
+    k64 = rng.integers(0, 10 * div, size=n, dtype=np.int64)
+    k64[: n // 2] = np.clip(rng.normal(4.3 * div, div / 100, size=n // 2), 4 * div, 5 * div - 1).astype(np.int64)
+    rng.shuffle(k64)
+    plan = check(k64, D, 2)
+    assert plan["split"][4] == 1
+    t64 = T(1)
+    keys = buckets([4 * 3 * t64] * 10, 6, 72)
+    keys[::2] = np.clip(rng.normal(3.5e5, 2e3, size=keys[::2].size), 3e5, 4e5 - 1).astype(np.int32)
+    tags = rng.integers(0, 2**62, size=keys.size, dtype=np.int64).astype(np.uint64)
+    dk = torch.from_numpy(keys).to(DEV)
+    dt = torch.from_numpy(tags.view(np.int64)).to(DEV)
+    hs.hs_sort_pairs(dk, dt, 6, 4)
+    torch.cuda.synchronize()
+    rk, rt = O.sort_pairs(keys, tags, 6, 4)
+    assert np.array_equal(dk.cpu().numpy(), rk)
+    assert np.array_equal(dt.cpu().numpy().view(np.uint64), rt)
