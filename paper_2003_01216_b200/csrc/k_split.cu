@@ -14,11 +14,10 @@
 //
 //   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
 //                    offsets; zeroes the count table
-//   k_split_sample   10 x 8 CTAs: fine-bin histograms of a 32k-key sample of
-//                    every candidate bucket
-//   k_split_map      one CTA per bucket: keeps equal-width sub-ranges unless
-//                    the sample's largest count is beyond the sampling noise
-//                    of a uniform bucket, else writes the equal-count map
+//   k_split_sample_map  one CTA per candidate bucket: fine-bin histogram of a
+//                    32k-key sample; keeps equal-width sub-ranges unless the
+//                    sample's largest count is beyond the sampling noise of a
+//                    uniform bucket, else writes the equal-count map
 //   k_split_count    persistent CTAs read slices (<= NT*VT keys of one chunk)
 //                    of S, count their sub-ranges in shared memory and add the
 //                    non-zero counts to the chunk's table row (next slice's
@@ -40,7 +39,7 @@
 // Sub-range of a key: min(mulhi(max(x - lo_b, 0), mul), nsb - 1) with mul =
 // floor((2^w - 1) / 10^(D-1)) nsb -- non-decreasing in the key, so sub-range
 // order is key order; keys clamped into bucket 0 / 9 (P:78 reading #3) land in
-// the first / last sub-range.  Skewed buckets (k_split_sample / k_split_map)
+// the first / last sub-range.  Skewed buckets (k_split_sample_map)
 // use equal-count groups of 8192 fine equal-width bins instead, picked from a
 // 32k-key sample: map[fine bin] is non-decreasing, so the order argument holds.
 // Roofline: HBM, 4 B read (count) + 8 B read+write (scatter) per int32 key.
@@ -124,15 +123,15 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
 
 // ------------------------------------------------------------------ sampled map
 // Equal-width sub-ranges fit keys spread over the digit range (C2, C3, C5, P3).
-// For a skewed bucket (C4: a normal peak) k_split_sample histograms a sample of
-// the bucket over kSplitFine fine bins, and k_split_map either keeps the equal-
+// For a skewed bucket (C4: a normal peak) k_split_sample_map histograms a sample
+// of the bucket over kSplitFine fine bins and either keeps the equal-
 // width sub-ranges (their largest sample count is within mean + 5 sqrt(mean))
 // or replaces them by equal-count groups of consecutive fine bins:
 // map[i] = floor(excl_prefix(i) * ns' / total), non-decreasing in i, so the
 // sub-range order is still key order.  The exact count pass decides as before
 // (an over-full sub-range -- e.g. one value with > T copies in a chunk -- makes
 // the bucket fall back).
-constexpr int kSampleCTAs = 8, kSamplePerCTA = 4096;  // 32k samples per candidate bucket
+constexpr int kSplitSamplesLog2 = 15, kSplitSamples = 1 << kSplitSamplesLog2;  // per candidate bucket
 
 template <typename K>
 __device__ __forceinline__ int fine_bin(K k, int shift, long long lo, unsigned long long fmul);
@@ -147,58 +146,49 @@ __device__ __forceinline__ int fine_bin<int64_t>(int64_t k, int shift, long long
     return (int)min((long long)__umul64hi((unsigned long long)d, fmul), (long long)(kSplitFine - 1));
 }
 
+// One CTA per candidate bucket: 32 sample loads per thread in flight, a
+// shared-memory fine-bin histogram, then the decision and the map.
 template <typename K>
-__global__ void __launch_bounds__(256) k_split_sample(const Ctl *__restrict__ ctl, const K *__restrict__ S,
-                                                      uint32_t *fhist) {
-    __shared__ uint32_t h[kSplitFine];
-    const int b = blockIdx.x / kSampleCTAs, part = blockIdx.x % kSampleCTAs;
-    const SplitCfg &C = ctl->split;
-    const Plan &P = ctl->plan;
-    if (!C.cand[b] || C.fmul[b] == 0) return;
-    for (int q = threadIdx.x; q < kSplitFine; q += blockDim.x) h[q] = 0;
-    __syncthreads();
-    const long long m = P.off[b + 1] - P.off[b], base = P.off[b];
-    const long long tot = (long long)kSampleCTAs * kSamplePerCTA;
-    const long long lo = C.lo[b];
-    const unsigned long long fmul = C.fmul[b];
-    const int shift = C.shift;
-    constexpr int PER = kSamplePerCTA / 256;
-    K kk[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {  // all loads in flight first
-        const long long r = (long long)part * kSamplePerCTA + j * 256 + threadIdx.x;  // evenly spaced positions
-        kk[j] = __ldg(S + base + (long long)((unsigned long long)r * (unsigned long long)m / (unsigned long long)tot));
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
-    __syncthreads();
-    uint32_t *const out = fhist + ((size_t)b * kSampleCTAs + part) * kSplitFine;  // this CTA's histogram
-    for (int q = threadIdx.x; q < kSplitFine; q += blockDim.x) out[q] = h[q];
-}
-
-__global__ void __launch_bounds__(1024) k_split_map(Ctl *ctl, const uint32_t *__restrict__ fhist, uint16_t *map,
-                                                    int tile_keys) {
-    constexpr int NT = 1024, PER = kSplitFine / NT;
-    static_assert(kSplitFine % NT == 0, "fine bins per thread");
-    __shared__ uint32_t est[kSplitFine];  // equal-width sub-range estimates (ns <= nsa <= kSplitFine)
+__global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__restrict__ S, uint16_t *map,
+                                                           int tile_keys) {
+    constexpr int NT = 1024, PER = kSplitFine / NT, SPT = kSplitSamples / NT;
+    static_assert(kSplitFine % NT == 0 && kSplitSamples % NT == 0, "per-thread shares");
+    __shared__ uint32_t h[kSplitFine];  // fine-bin histogram, then the equal-width estimates
     __shared__ uint32_t wsum[NT / 32];
     __shared__ unsigned s_max;
     Plan &P = ctl->plan;
     SplitCfg &C = ctl->split;
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (!C.cand[b] || C.fmul[b] == 0) return;
+    const long long m = P.off[b + 1] - P.off[b], base = P.off[b];
+    const long long lo = C.lo[b];
+    const unsigned long long fmul = C.fmul[b];
+    const int shift = C.shift;
     const int ns = P.nsb[b];
-    uint32_t h[PER], sum = 0;
+    for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
+    if (tid == 0) s_max = 0;
+    __syncthreads();
+    constexpr int R = 16;  // samples per round and thread (loads of a round in flight together)
+    static_assert(SPT % R == 0, "sample rounds");
+#pragma unroll 1
+    for (int j0 = 0; j0 < SPT; j0 += R) {
+        K kk[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {  // evenly spaced positions of the bucket
+            const unsigned long long r = (unsigned long long)((j0 + j) * NT + tid);
+            kk[j] = __ldg(S + base + (long long)((r * (unsigned long long)m) >> kSplitSamplesLog2));
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
+    }
+    __syncthreads();
+    uint32_t hv[PER], sum = 0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        h[j] = 0;
-        for (int part = 0; part < kSampleCTAs; ++part)  // sum of the sampling CTAs' histograms
-            h[j] += fhist[((size_t)b * kSampleCTAs + part) * kSplitFine + tid * PER + j];
-        sum += h[j];
+        hv[j] = h[tid * PER + j];
+        sum += hv[j];
     }
-    for (int q = tid; q < ns; q += NT) est[q] = 0;
-    if (tid == 0) s_max = 0;
-    // block exclusive scan of the per-thread sums
+    // block exclusive scan of the per-thread sums (its barrier also frees h for the estimates)
     uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -211,10 +201,13 @@ __global__ void __launch_bounds__(1024) k_split_map(Ctl *ctl, const uint32_t *__
     const uint32_t excl0 = incl - sum + __reduce_add_sync(0xffffffffu, wl);
     const uint32_t wt = lane < NT / 32 ? wsum[lane] : 0u;
     const uint32_t total = __reduce_add_sync(0xffffffffu, wt);
+    uint32_t *const est = h;  // equal-width sub-range estimates (ns <= nsa <= kSplitFine)
+    for (int q = tid; q < ns; q += NT) est[q] = 0;
+    __syncthreads();
     // equal-width estimate: fine bin i lies (about) in sub-range floor(i ns / kSplitFine)
 #pragma unroll
     for (int j = 0; j < PER; ++j)
-        if (h[j]) atomicAdd(&est[(tid * PER + j) * ns / kSplitFine], h[j]);
+        if (hv[j]) atomicAdd(&est[(tid * PER + j) * ns / kSplitFine], hv[j]);
     __syncthreads();
     for (int q = tid; q < ns; q += NT) atomicMax(&s_max, est[q]);
     __syncthreads();
@@ -224,7 +217,7 @@ __global__ void __launch_bounds__(1024) k_split_map(Ctl *ctl, const uint32_t *__
     const float mean_s = (float)total / (float)ns;
     const bool skewed = total > 0 && (float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f;
     if (!skewed) return;  // mode stays 0
-    const long long c = 1LL << P.log2c, m = P.off[b + 1] - P.off[b], cm = (m + c - 1) / c;
+    const long long c = 1LL << P.log2c, cm = (m + c - 1) / c;
     const long long tm = split_target_map(tile_keys);
     long long ns2 = (cm + tm - 1) / tm;
     if (ns2 > C.nsa[b]) ns2 = C.nsa[b];
@@ -234,7 +227,7 @@ __global__ void __launch_bounds__(1024) k_split_map(Ctl *ctl, const uint32_t *__
     for (int j = 0; j < PER; ++j) {
         const long long g = (long long)run * ns2 / total;
         map[b * kSplitFine + tid * PER + j] = (uint16_t)(g < ns2 - 1 ? g : ns2 - 1);
-        run += h[j];
+        run += hv[j];
     }
     if (tid == 0) {
         P.nsb[b] = (int)ns2;
@@ -571,7 +564,7 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
 
 // ------------------------------------------------------------------ host
 // words after the split table: fine histograms (u32) and sampled maps (u16) of the 10 buckets
-constexpr long long kSplitExtraWords = 10LL * kSampleCTAs * kSplitFine + 10LL * kSplitFine / 2;
+constexpr long long kSplitExtraWords = 10LL * kSplitFine / 2;
 
 long long split_table_words(long long n, int log2c, int tile_keys) {
     return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + kSplitExtraWords;
@@ -606,13 +599,11 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     const long long c = 1LL << log2c;
     const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
     const long long tab_cap = tab_words - kSplitExtraWords;
-    uint32_t *const fhist = tab + tab_cap;
-    uint16_t *const map = reinterpret_cast<uint16_t *>(fhist + 10 * kSampleCTAs * kSplitFine);
+    uint16_t *const map = reinterpret_cast<uint16_t *>(tab + tab_cap);
     prof_begin(kProfPlan, st);
     k_split_setup<<<1, 1024, 0, st>>>(ctl, div, 8 * (int)sizeof(K), key_shift, tile_keys, TS, tab_cap, nsb_cap,
                                       tab);
-    k_split_sample<K><<<10 * kSampleCTAs, 256, 0, st>>>(ctl, S, fhist);
-    k_split_map<<<10, 1024, 0, st>>>(ctl, fhist, map, tile_keys);
+    k_split_sample_map<K><<<10, 1024, 0, st>>>(ctl, S, map, tile_keys);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
@@ -625,7 +616,7 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
     ks<<<(unsigned)sgrid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap, map);
     prof_end(kProfSplitScatter, st);
-    *launches += 6;
+    *launches += 5;
     return cudaGetLastError();
 }
 
