@@ -270,6 +270,25 @@ int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chu
                    int *levels_out, int *tile_levels_out);
 
 /*
+ * a4-a7 on keys already partitioned by leading digit (hs_msd_partition's
+ * output, or the buckets a rank receives in the f2 exchange): sort every
+ * bucket in place -- the same chunk sort (with the K5a value split) and chunk
+ * tree merge as hs_sort, without the partition.  The result equals
+ * hs_merge(hs_sort_chunks(keys)) for the same offsets (each bucket ascending,
+ * buckets left where they are).
+ *
+ *   keys[n]            in/out: device.
+ *   num_digits         D of the keys (the split uses bucket b's digit range
+ *                      [b 10^(D-1), (b+1) 10^(D-1)); keys outside it are still
+ *                      sorted correctly, only the split may fall back).
+ *   bucket_offsets[11] in: device int64 CSR offsets, [0] = 0, [10] = n,
+ *                      non-decreasing; NOT checked (it lives on the device).
+ *   chunks_per_bucket  c, power of two in [1, 65536].
+ */
+hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, const int64_t *bucket_offsets,
+                            int chunks_per_bucket, cudaStream_t stream);
+
+/*
  * The device plan hs_sort would run on keys (bench / tests: which buckets the
  * K5a value split takes, hence how many merge levels run).  Runs the
  * partition and the split into scratch memory (keys is not modified),

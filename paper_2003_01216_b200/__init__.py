@@ -19,7 +19,7 @@ from . import _build
 
 __all__ = [
     "HS_INT32", "HS_INT64", "HybridSortError", "library_path", "load",
-    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_plan", "hs_sort_host",
+    "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_plan", "hs_sort_buckets", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
     "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan", "SortGraph",
@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
     "hs_msd_partition_pairs", "hs_sort_pairs",
     "hs_partition_plan_create", "hs_partition_scatter", "hs_partition_plan_destroy", "hs_sort_plan",
+    "hs_sort_buckets",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy",
                  "split_count", "split_scatter")
@@ -68,10 +69,11 @@ def load(path: str | None = None):
     lib.hs_sort.argtypes = [vp, i64, ci, ci, ci, vp]
     lib.hs_sort_shared.argtypes = [vp, i64, ci, ci, vp]
     lib.hs_sort_plan.argtypes = [vp, i64, ci, ci, ci, vp, vp, vp, vp]
+    lib.hs_sort_buckets.argtypes = [vp, i64, ci, ci, vp, ci, vp]
     lib.hs_msd_partition_pairs.argtypes = [vp, vp, i64, ci, vp, vp, vp, vp]
     lib.hs_sort_pairs.argtypes = [vp, vp, i64, ci, ci, vp]
     for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared",
-              "hs_msd_partition_pairs", "hs_sort_pairs", "hs_sort_plan"):
+              "hs_msd_partition_pairs", "hs_sort_pairs", "hs_sort_plan", "hs_sort_buckets"):
         getattr(lib, f).restype = ci
     lib.hs_status_string.argtypes = [ci]
     lib.hs_status_string.restype = ctypes.c_char_p
@@ -265,6 +267,21 @@ def hs_sort(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None, vali
         _validate_range(keys, num_digits)
     with torch.cuda.device(keys.device):
         _check(load().hs_sort(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket, _stream(stream)))
+    return keys
+
+
+def hs_sort_buckets(keys, bucket_offsets, num_digits: int, chunks_per_bucket: int = 8, stream=None):
+    """Sort every bucket of an already digit-partitioned array in place (a4-a7 of hs_sort
+    without the partition; the f2 receive side).  bucket_offsets: device int64[11]."""
+    torch = _torch()
+    _check_tensor(keys, "keys")
+    dt = _dtype_code(keys)
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11 or bucket_offsets.device != keys.device:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 entries on the keys' device")
+    off = bucket_offsets.contiguous()
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort_buckets(keys.data_ptr(), keys.numel(), dt, num_digits, off.data_ptr(),
+                                      chunks_per_bucket, _stream(stream)))
     return keys
 
 

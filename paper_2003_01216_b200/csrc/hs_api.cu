@@ -429,8 +429,12 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
 namespace {
 
 // a1-a7 on validated arguments (n > 0).  key_shift as partition_impl.
+// user_off (device int64[11], hs_sort_buckets): keys are already partitioned by
+// digit into those buckets -- a1-a3 are skipped, the plan comes from user_off,
+// the split reads keys and writes the scratch, the tile sort reads both.
 hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
-                      int log2c, cudaStream_t stream, int *launches_out, hs::Plan *inspect = nullptr) {
+                      int log2c, cudaStream_t stream, int *launches_out, hs::Plan *inspect = nullptr,
+                      const int64_t *user_off = nullptr) {
     hs_status_t s;
     int sms;
     cudaError_t e = device_setup(&sms);
@@ -474,19 +478,29 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
-    // a1-a3: tile histograms, lookback prefix (+ offsets + plan), stable scatter keys -> S
-    HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
-                                     ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift),
-                "K1-K3 partition");
-    launches += 2;
-    // a5 (K5a): value split of every chunk that exceeds one tile, S -> keys
+    // where the partitioned keys are (part) and where the split writes (spl)
+    void *part = ws.S, *spl = keys;
+    if (user_off) {
+        // a4: plan from the caller's bucket offsets (keys already partitioned)
+        HS_TRY_CUDA(hs::launch_plan((const long long *)user_off, ws.ctl, log2c, hs::kPlanSort, T, stream), "K4 plan");
+        ++launches;
+        part = keys;
+        spl = ws.S;
+    } else {
+        // a1-a3: tile histograms, lookback prefix (+ offsets + plan), stable scatter keys -> S
+        HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                         ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift),
+                    "K1-K3 partition");
+        launches += 2;
+    }
+    // a5 (K5a): value split of every chunk that exceeds one tile, part -> spl
     if (split_on)
-        HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, ws.S, keys, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
+        HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, part, spl, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
                                      key_shift, &launches, stream),
                     "K5a split");
-    // a5: leaf-tile sort (S, or keys for split buckets) -> (keys | S) per bucket parity
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, ws.S, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
-                                     ws.sbtab, &ws.ctl->split),
+    // a5: leaf-tile sort (part, or spl for split buckets) -> (keys | S) per bucket parity
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
+                                     ws.sbtab, &ws.ctl->split, spl),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
@@ -522,6 +536,30 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
     }
     int launches = 0;
     if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) return s;
+    g_launches = launches;
+    g_err[0] = 0;
+    return HS_OK;
+}
+
+hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, const int64_t *bucket_offsets,
+                            int chunks_per_bucket, cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if (!bucket_offsets || ((uintptr_t)bucket_offsets & 7) != 0)
+        return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL or not 8-byte aligned");
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int launches = 0;
+    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches, nullptr,
+                       bucket_offsets)) != HS_OK)
+        return s;
     g_launches = launches;
     g_err[0] = 0;
     return HS_OK;

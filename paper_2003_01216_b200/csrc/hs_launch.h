@@ -35,7 +35,7 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 struct SplitCfg;
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr,
-                             const SplitCfg *scfg = nullptr);
+                             const SplitCfg *scfg = nullptr, const void *src_split = nullptr);  // null: F
 
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +

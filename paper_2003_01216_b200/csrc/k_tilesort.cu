@@ -151,7 +151,7 @@ struct TSGeo {
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp, const uint32_t *__restrict__ sbtab,
-                                                        const SplitCfg *__restrict__ scfg) {
+                                                        const SplitCfg *__restrict__ scfg, const K *src_split) {
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
@@ -181,13 +181,13 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     bool frac = false;
     U f_base = 0, f_mul = 0;
     int f_sft = 0;
-    if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (already in F)
+    if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (in src_split)
         const int ns = P.nsb[b];
         const long long j = (unsigned)i / (unsigned)ns, t = i - j * ns;  // i < c * ns < 2^31
         const uint32_t *e = sbtab + P.sboff[b] + j * (ns + 1) + t;
         lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
         len = (int)(__ldg(e + 1) - __ldg(e));
-        src = F;
+        src = src_split;
         const U mul = (U)scfg->mul[b];
         if (scfg->mode[b] == 0 && t > 0 && t < ns - 1 && mul <= (U)(~(U)0 >> 12)) {
             frac = true;
@@ -545,7 +545,7 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
-                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg) {
+                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
@@ -559,15 +559,17 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
-    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab, scfg);
+    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab, scfg,
+                                                    (const K *)(src_split ? src_split : F));
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
-                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg);
+                             long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg,
+                             const void *src_split) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split);
 }
 
 }  // namespace hs

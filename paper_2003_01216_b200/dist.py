@@ -34,8 +34,8 @@ more than 10 ranks the extra ranks own no digit (at most ten nodes).
 rank's K3 stores every digit's keys straight into the owner rank's
 symmetric-memory receive buffer over NVLink (hs_partition_scatter with peer
 destination pointers), so step 4 costs no collective call and no staging copy,
-and the owner's buffer arrives already partitioned by digit (steps 5 is then
-chunk sort + tree merge, no second MSD pass).
+and the owner's buffer arrives already partitioned by digit (step 5 is then
+hs_sort_buckets: chunk sort + tree merge, no second MSD pass).
 
 In ``dist_sort`` the per-rank steps 1 and 5 are injected as ``ops`` so the host logic
 can be tested on CPU with the gloo backend (tests/test_dist.py passes
@@ -46,7 +46,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import PartitionPlan, assign_buckets, hs_merge, hs_msd_partition, hs_sort, hs_sort_chunks
+from . import PartitionPlan, assign_buckets, hs_msd_partition, hs_sort, hs_sort_buckets
 
 
 @dataclass
@@ -217,8 +217,7 @@ def dist_sort_fused(keys, num_digits: int, chunks: int = 8, group=None):
     local = buf[:n_local]
     if n_local:
         roff = torch.tensor(recv_offsets[rank], dtype=torch.int64, device=keys.device)
-        hs_sort_chunks(local, roff, chunks, out=local)
-        hs_merge(local, roff, chunks, out=local)
+        hs_sort_buckets(local, roff, num_digits, chunks)  # chunk sort (+ value split) + tree merge, in place
     send = [sum(sizes[rank][d] for d in range(10) if owner[d] == g) for g in range(world)]
     recv = [sum(sizes[r][d] for d in range(10) if owner[d] == rank) for r in range(world)]
     return local, DistInfo(group_start, global_sizes, send, recv, max_load)

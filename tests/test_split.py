@@ -211,3 +211,34 @@ def test_split_sampled_map_int64_and_pairs():
     rk, rt = O.sort_pairs(keys, tags, 6, 4)
     assert np.array_equal(dk.cpu().numpy(), rk)
     assert np.array_equal(dt.cpu().numpy().view(np.uint64), rt)
+
+
+@pytest.mark.parametrize("name,n,c", [("C1", None, 8), ("C4", 3_000_000, 8), ("C2", 4_000_000, 2), ("C5", 2_000_001, 4)])
+def test_sort_buckets_after_partition(name, n, c):
+    """hs_sort_buckets (a4-a7 on a digit-partitioned array, the f2 receive side) == oracle sort of
+    the keys == hs_merge(hs_sort_chunks(.)) on the same partition."""
+    cfg = W.CONFIGS[name]
+    keys = W.generate(name, 0, n)
+    part, off = hs.hs_msd_partition(torch.from_numpy(keys).to(DEV), cfg.num_digits)
+    ref_cm = hs.hs_merge(hs.hs_sort_chunks(part.clone(), off, c), off, c)
+    hs.hs_sort_buckets(part, off, cfg.num_digits, c)
+    torch.cuda.synchronize()
+    got = part.cpu().numpy()
+    assert np.array_equal(got, O.sort(keys, cfg.num_digits, c))
+    assert np.array_equal(got, ref_cm.cpu().numpy())
+
+
+def test_sort_buckets_misaligned_and_empty():
+    t = T(0)
+    keys = buckets([3 * t + b for b in range(10)], 8, 81)
+    base = torch.from_numpy(np.concatenate([[7], keys, [9]]).astype(np.int32)).to(DEV)
+    part, off = hs.hs_msd_partition(base[1:-1].clone(), 8)
+    view = base[1:-1]
+    view.copy_(part)
+    hs.hs_sort_buckets(view, off, 8, 1)
+    torch.cuda.synchronize()
+    got = base.cpu().numpy()
+    assert got[0] == 7 and got[-1] == 9
+    assert np.array_equal(got[1:-1], np.sort(keys))
+    e = torch.empty(0, dtype=torch.int32, device=DEV)
+    hs.hs_sort_buckets(e, torch.zeros(11, dtype=torch.int64, device=DEV), 8, 8)
