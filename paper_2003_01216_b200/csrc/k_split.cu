@@ -52,9 +52,18 @@ namespace hs {
 
 template <typename K>
 struct SplGeo;
+#ifndef HS_SPL_VT
+#define HS_SPL_VT 16
+#endif
+#ifndef HS_SPL_MINB_SCAT
+#define HS_SPL_MINB_SCAT 2
+#endif
+#ifndef HS_SPL_MINB_COUNT
+#define HS_SPL_MINB_COUNT 3
+#endif
 template <>
 struct SplGeo<int32_t> {
-    static constexpr int NT = 512, VT = 16, MINB_COUNT = 3, MINB_SCAT = 2;
+    static constexpr int NT = 512, VT = HS_SPL_VT, MINB_COUNT = HS_SPL_MINB_COUNT, MINB_SCAT = HS_SPL_MINB_SCAT;
 };
 template <>
 struct SplGeo<int64_t> {
