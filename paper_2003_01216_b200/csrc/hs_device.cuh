@@ -72,6 +72,29 @@ __device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &
     return (int)(q < 9ull ? q : 9ull);
 }
 
+// Programmatic dependent launch (PDL): the kernels of hs_sort after K1 are
+// launched with programmatic stream serialization, so each may be scheduled
+// while its predecessor drains; every such kernel calls griddep_wait() first
+// (full completion + memory flush of the predecessor) before touching memory.
+// A no-op for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------------- plan
 // Geometry of one call, computed on the device (no host sync).
 //  * bucket b = [off[b], off[b+1]).

@@ -40,6 +40,7 @@
 
 namespace hs {
 
+
 template <typename K>
 struct MGeo;
 template <>
@@ -83,6 +84,7 @@ template <typename K>
 __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
                                   const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds) {
     constexpr long long Q = kSampleQ;
+    griddep_wait();
     if (level >= __ldg(&plan_g->Lmax)) return;  // no bucket runs this level (the host only knows a bound)
     __shared__ Plan P;
     load_plan_m(P, plan_g);
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     const int tid = threadIdx.x;
     const K kMax = KeyTraits<K>::kMax;
 
+    griddep_wait();
     if (level >= __ldg(&plan_g->Lmax)) return;  // whole CTA: nothing at this level
     load_plan_m(P, plan_g);
     if (tid == 0) {
@@ -437,18 +440,34 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
     const int nbounds = nblocks + 1;
+    // both kernels of a level are launched with programmatic stream serialization:
+    // each may be scheduled while its predecessor drains (an empty level past the
+    // device plan then costs little more than its launch) and waits in griddep_wait
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     prof_begin(kProfMergePartition, st);
-    k_merge_partition<K><<<(unsigned)((nbounds + 127) / 128), 128, 0, st>>>(
-        plan, (K *)F, (K *)S, (const K *)src0, (const K *)samp_in, corank, level, n, TM, nbounds);
+    cfg.gridDim = dim3((unsigned)((nbounds + 127) / 128));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_merge_partition<K>, plan, (K *)F, (K *)S, (const K *)src0,
+                                       (const K *)samp_in, corank, level, n, TM, nbounds);
     prof_end(kProfMergePartition, st);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     long long grid = (long long)per_sm * num_sms;
     if (grid > nblocks) grid = nblocks;
     prof_begin(kProfMergeLevel, st);
-    kern<<<(unsigned)grid, G::kNT + 32, SM::bytes(), st>>>(plan, (K *)F, (K *)S, (const K *)src0, corank,
-                                                           (K *)samp_out, level, n, nblocks);
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(G::kNT + 32);
+    cfg.dynamicSmemBytes = SM::bytes();
+    e = cudaLaunchKernelEx(&cfg, kern, plan, (K *)F, (K *)S, (const K *)src0, (const int *)corank, (K *)samp_out,
+                           level, n, nblocks);
     prof_end(kProfMergeLevel, st);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kScanNT) k_tile_scan(const uint32_t *__restric
                                                        uint32_t *__restrict__ tile_pref, int ntiles,
                                                        unsigned long long *status, Ctl *ctl, long long *user_off,
                                                        int plan_mode, int log2c, int tile_keys) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int NW = kScanNT / 32;
     __shared__ unsigned s_wtot[NW][10];
     __shared__ unsigned s_cta_excl[10];
@@ -424,6 +425,7 @@ template <typename K, int NT, int VT, bool TABLE>
 __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *__restrict__ out, int n, int h,
                                                 DigitParams<K> dp, const Ctl *__restrict__ ctl,
                                                 const uint32_t *__restrict__ tile_pref, int ntiles, DstTable<K> dtab) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int T = NT * VT;
     constexpr int NW = NT / 32;
     static_assert(VT <= 16 && T <= 16384, "packing limits");
@@ -513,10 +515,10 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     cudaError_t e = cudaSuccess;
     if (do_count) {
         prof_begin(kProfTileScan, st);
-        k_tile_scan<<<sgrid, kScanNT, 0, st>>>(tile_hist, tile_pref, (int)ntiles, status, ctl, user_off, plan_mode,
-                                               log2c, sort_tile_keys);
+        e = launch_pdl(k_tile_scan, dim3(sgrid), dim3(kScanNT), 0, st, tile_hist, tile_pref, (int)ntiles, status, ctl,
+                       user_off, plan_mode, log2c, sort_tile_keys);
         prof_end(kProfTileScan, st);
-        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
     }
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
@@ -542,8 +544,9 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     DstTable<K> dtab;
     dtab.use = dst10 != nullptr;
     for (int d = 0; d < 10; ++d) dtab.dst[d] = dst10 ? (K *)dst10[d] : nullptr;
-    kern<<<(unsigned)grid, G::kScatNT, SS::bytes(), st>>>((const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
+cudaError_t el = launch_pdl(kern, dim3((unsigned)grid), dim3(G::kScatNT), SS::bytes(), st, (const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
                                                           (int)ntiles, dtab);
+    if (el != cudaSuccess) return el;
     prof_end(kProfScatter, st);
     return cudaGetLastError();
 }

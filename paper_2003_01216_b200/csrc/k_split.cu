@@ -81,6 +81,7 @@ __host__ __device__ __forceinline__ long long split_target_map(int tile_keys) { 
 
 __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, int key_shift, int tile_keys,
                               int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ long long s_words;
     if (threadIdx.x == 0) {
         Plan &P = ctl->plan;
@@ -160,6 +161,7 @@ __device__ __forceinline__ int fine_bin<int64_t>(int64_t k, int shift, long long
 template <typename K>
 __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__restrict__ S, uint16_t *map,
                                                            int tile_keys) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int NT = 1024, PER = kSplitFine / NT, SPT = kSplitSamples / NT;
     static_assert(kSplitFine % NT == 0 && kSplitSamples % NT == 0, "per-thread shares");
     __shared__ uint32_t h[kSplitFine];  // fine-bin histogram, then the equal-width estimates
@@ -333,6 +335,7 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                           uint32_t *tab, int nsb_cap, const uint16_t *map) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int TS = NT * VT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
@@ -403,6 +406,7 @@ template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                             K *__restrict__ F, uint32_t *cur, int nsb_cap,
                                                             const uint16_t *map) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int TS = NT * VT;
     constexpr bool PACK = sizeof(K) == 4;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
@@ -520,6 +524,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
 
 // ------------------------------------------------------------- per-chunk scan
 __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t *tab, uint32_t *cur, int tile_keys) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ uint32_t wsum[kSplitPlanNT / 32];
     __shared__ bool s_last;
     Plan &P = ctl->plan;
@@ -610,20 +615,27 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     const long long tab_cap = tab_words - kSplitExtraWords;
     uint16_t *const map = reinterpret_cast<uint16_t *>(tab + tab_cap);
     prof_begin(kProfPlan, st);
-    k_split_setup<<<1, 1024, 0, st>>>(ctl, div, 8 * (int)sizeof(K), key_shift, tile_keys, TS, tab_cap, nsb_cap,
-                                      tab);
-    k_split_sample_map<K><<<10, 1024, 0, st>>>(ctl, S, map, tile_keys);
+    if ((e = launch_pdl(k_split_setup, dim3(1), dim3(1024), 0, st, ctl, div, 8 * (int)sizeof(K), key_shift,
+                        tile_keys, TS, tab_cap, nsb_cap, tab)) != cudaSuccess)
+        return e;
+    if ((e = launch_pdl(k_split_sample_map<K>, dim3(10), dim3(1024), 0, st, ctl, S, map, tile_keys)) != cudaSuccess)
+        return e;
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
-    kc<<<(unsigned)pgrid, G::NT, sm_count, st>>>(ctl, S, tab, nsb_cap, map);
+    if ((e = launch_pdl(kc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map)) != cudaSuccess)
+        return e;
     prof_end(kProfSplitCount, st);
     prof_begin(kProfPlan, st);
-    k_split_plan<<<(unsigned)(10 * c), kSplitPlanNT, 0, st>>>(ctl, tab, cur, tile_keys);
+    if ((e = launch_pdl(k_split_plan, dim3((unsigned)(10 * c)), dim3(kSplitPlanNT), 0, st, ctl, tab, cur,
+                        tile_keys)) != cudaSuccess)
+        return e;
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
     const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
-    ks<<<(unsigned)sgrid, G::NT, sm_scat, st>>>(ctl, S, F, cur, nsb_cap, map);
+    if ((e = launch_pdl(ks, dim3((unsigned)sgrid), dim3(G::NT), sm_scat, st, ctl, S, F, cur, nsb_cap, map)) !=
+        cudaSuccess)
+        return e;
     prof_end(kProfSplitScatter, st);
     *launches += 5;
     return cudaGetLastError();

@@ -73,6 +73,7 @@ __device__ __forceinline__ void load_plan(Plan &dst, const Plan *src) {
 
 // =================================================================== K4
 __global__ void k_plan(const long long *__restrict__ user_off, Ctl *ctl, int log2c, int mode, int tile_keys) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         long long off[11];
         for (int b = 0; b < 11; ++b) off[b] = user_off[b];
@@ -82,6 +83,7 @@ __global__ void k_plan(const long long *__restrict__ user_off, Ctl *ctl, int log
 
 // K4 for hs_sort_shared (no MSD step): the whole array is bucket 0.
 __global__ void k_plan_whole(Ctl *ctl, long long n, int log2c, int tile_keys) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         long long off[11];
         off[0] = 0;
@@ -152,6 +154,7 @@ template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp, const uint32_t *__restrict__ sbtab,
                                                         const SplitCfg *__restrict__ scfg, const K *src_split) {
+    griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
@@ -531,14 +534,16 @@ int sort_tile_keys(int dt) {
 
 cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode, int tile_keys, cudaStream_t st) {
     prof_begin(kProfPlan, st);
-    k_plan<<<1, 32, 0, st>>>(user_off, ctl, log2c, mode, tile_keys);
+    cudaError_t e = launch_pdl(k_plan, dim3(1), dim3(32), 0, st, user_off, ctl, log2c, mode, tile_keys);
+    if (e != cudaSuccess) return e;
     prof_end(kProfPlan, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st) {
     prof_begin(kProfPlan, st);
-    k_plan_whole<<<1, 32, 0, st>>>(ctl, n, log2c, tile_keys);
+    cudaError_t e = launch_pdl(k_plan_whole, dim3(1), dim3(32), 0, st, ctl, n, log2c, tile_keys);
+    if (e != cudaSuccess) return e;
     prof_end(kProfPlan, st);
     return cudaGetLastError();
 }
@@ -559,8 +564,9 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
-    kern<<<(unsigned)max_tiles, G::kNT, smem, st>>>(plan, (const K *)src, (K *)F, (K *)S, (K *)samp, sbtab, scfg,
-                                                    (const K *)(src_split ? src_split : F));
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)max_tiles), dim3(G::kNT), smem, st, plan, (const K *)src, (K *)F,
+                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F));
+    if (e != cudaSuccess) return e;
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
 }

@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/e7
-python tools/exp.py run main spl8 spl12 > gpurun_out/e7/exp.log 2>&1
-python tools/exp.py run main spl8 spl12 >> gpurun_out/e7/exp.log 2>&1
+mkdir -p gpurun_out/e8
+python tools/exp.py run main pdl > gpurun_out/e8/exp.log 2>&1
+python tools/exp.py run main pdl >> gpurun_out/e8/exp.log 2>&1
