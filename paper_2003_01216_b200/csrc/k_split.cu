@@ -65,9 +65,12 @@ template <>
 struct SplGeo<int32_t> {
     static constexpr int NT = 512, VT = HS_SPL_VT, MINB_COUNT = HS_SPL_MINB_COUNT, MINB_SCAT = HS_SPL_MINB_SCAT;
 };
+#ifndef HS_SPL_VT64
+#define HS_SPL_VT64 8
+#endif
 template <>
 struct SplGeo<int64_t> {
-    static constexpr int NT = 512, VT = 8, MINB_COUNT = 3, MINB_SCAT = 2;
+    static constexpr int NT = 512, VT = HS_SPL_VT64, MINB_COUNT = 3, MINB_SCAT = 2;
 };
 constexpr int kSplitMaxSub = 4096;  // sub-ranges per chunk (shared-memory counters)
 constexpr int kSplitPlanNT = 512;
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int NT = 1024, PER = kSplitFine / NT, SPT = kSplitSamples / NT;
     static_assert(kSplitFine % NT == 0 && kSplitSamples % NT == 0, "per-thread shares");
-    __shared__ uint32_t h[kSplitFine];  // fine-bin histogram, then the equal-width estimates
+    __shared__ uint32_t h[kSplitFine + 1];  // fine-bin histogram, then its exclusive prefix (+ total)
     __shared__ uint32_t wsum[NT / 32];
     __shared__ unsigned s_max;
     Plan &P = ctl->plan;
@@ -212,15 +215,29 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
     const uint32_t excl0 = incl - sum + __reduce_add_sync(0xffffffffu, wl);
     const uint32_t wt = lane < NT / 32 ? wsum[lane] : 0u;
     const uint32_t total = __reduce_add_sync(0xffffffffu, wt);
-    uint32_t *const est = h;  // equal-width sub-range estimates (ns <= nsa <= kSplitFine)
-    for (int q = tid; q < ns; q += NT) est[q] = 0;
-    __syncthreads();
-    // equal-width estimate: fine bin i lies (about) in sub-range floor(i ns / kSplitFine)
+    // h <- exclusive prefix of the fine bins (everyone read its hv before the scan's barrier)
+    {
+        uint32_t run0 = excl0;
 #pragma unroll
-    for (int j = 0; j < PER; ++j)
-        if (hv[j]) atomicAdd(&est[(tid * PER + j) * ns / kSplitFine], hv[j]);
+        for (int j = 0; j < PER; ++j) {
+            h[tid * PER + j] = run0;
+            run0 += hv[j];
+        }
+        if (tid == 0) h[kSplitFine] = total;
+    }
     __syncthreads();
-    for (int q = tid; q < ns; q += NT) atomicMax(&s_max, est[q]);
+    // equal-width sub-range t holds (about) the fine bins i with floor(i ns / kSplitFine) = t,
+    // i.e. [ceil(t F / ns), ceil((t+1) F / ns)): its sample count is a prefix difference
+    {
+        uint32_t mx = 0;
+        for (int t = tid; t < ns; t += NT) {
+            const int lo_i = (t * kSplitFine + ns - 1) / ns, hi_i = ((t + 1) * kSplitFine + ns - 1) / ns;
+            const uint32_t e = h[hi_i] - h[lo_i];
+            mx = e > mx ? e : mx;
+        }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) atomicMax(&s_max, mx);
+    }
     __syncthreads();
     // keep equal width unless the largest sample count is beyond the sampling noise of a
     // uniform bucket: > mean + 5 sqrt(mean) + 1 (mean = total / ns samples per sub-range;

@@ -1,7 +1,11 @@
-mkdir -p gpurun_out/s24
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s24/tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/s24/tests.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s24/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/s24/smoke.log
-for c in C3 C4 C5 C1; do
-  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline >> gpurun_out/s24/b_$c.json 2>> gpurun_out/s24/b_$c.log
-done
-timeout 300 python bench.py --dist --fused --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s24/b_distf.json 2> gpurun_out/s24/b_distf.log
+mkdir -p gpurun_out/s25
+python tools/exp.py run main --cfg C4 > gpurun_out/s25/exp.log 2>&1
+python tools/exp.py run main >> gpurun_out/s25/exp.log 2>&1
+timeout 600 python -m pytest tests/test_split.py -x -q > gpurun_out/s25/split.log 2>&1; echo "rc=$?" >> gpurun_out/s25/split.log
+python - > gpurun_out/s25/plans.log 2>&1 <<'PY'
+import torch, workload as W, paper_2003_01216_b200 as hs
+for c in ["C3", "C4", "C5", "C2", "P3"]:
+    cfg = W.CONFIGS[c]
+    d = torch.from_numpy(W.generate(c)).cuda()
+    print(c, hs.hs_sort_plan(d, cfg.num_digits, cfg.chunks))
+PY
