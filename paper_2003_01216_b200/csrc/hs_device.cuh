@@ -130,6 +130,7 @@ struct Plan {
 // range, the unit of the sampled sub-range map of skewed buckets (fine enough
 // that one bin near a C4-like peak holds ~0.06 T keys of a chunk).
 constexpr int kSplitFine = 8192;
+constexpr int kMapChunksMax = 64;  // per-chunk sampled maps up to this many chunks per bucket
 struct SplitCfg {
     long long slice_prefix[11];  // CTAs of the count / scatter passes per bucket (c * spc[b])
     long long lo[10];            // bucket b's value range starts at b * 10^(D-1)
@@ -139,6 +140,8 @@ struct SplitCfg {
     int cand[10];                // bucket b is split if no sub-range of its chunks exceeds T
     int mode[10];                // 0: equal-width sub-ranges (mul); 1: sub-range = map[b][fine bin] (skewed bucket)
     int nsa[10];                 // split-table row capacity per chunk - 1 (nsb[b] <= nsa[b])
+    int ns0[10];                 // equal-width sub-ranges per chunk (nsb[b] before any map)
+    int map_chunks;              // sampled maps per bucket: c (one per chunk) or 1 (c > kMapChunksMax)
     unsigned bad;                // buckets with an over-full sub-range (fall back to merge levels)
     unsigned ticket;
     int shift;                   // sort key of an item = item >> shift (hs_sort_pairs)

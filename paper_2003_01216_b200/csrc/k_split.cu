@@ -14,10 +14,11 @@
 //
 //   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
 //                    offsets; zeroes the count table
-//   k_split_sample_map  one CTA per candidate bucket: fine-bin histogram of a
-//                    32k-key sample; keeps equal-width sub-ranges unless the
-//                    sample's largest count is beyond the sampling noise of a
-//                    uniform bucket, else writes the equal-count map
+//   k_split_sample_map  one CTA per chunk of a candidate bucket: fine-bin
+//                    histogram of a 32k-key sample of the chunk and its equal-
+//                    count map; the bucket keeps equal-width sub-ranges unless
+//                    some chunk's largest sample count is beyond the sampling
+//                    noise of a uniform range (then every chunk uses its map)
 //   k_split_count    persistent CTAs read slices (<= NT*VT keys of one chunk)
 //                    of S, count their sub-ranges in shared memory and add the
 //                    non-zero counts to the chunk's table row (next slice's
@@ -110,6 +111,7 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
                 C.spc[b] = (int)spc;
                 acc_s += c * spc;
                 P.nsb[b] = (int)ns;
+                C.ns0[b] = (int)ns;
                 C.nsa[b] = (int)nsa;
                 P.sboff[b] = acc_t;
                 acc_t += c * (nsa + 1);
@@ -128,6 +130,7 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
         }
         C.slice_prefix[10] = acc_s;
         C.shift = key_shift;
+        C.map_chunks = c <= kMapChunksMax ? (int)c : 1;
         s_words = acc_t;
     }
     __syncthreads();
@@ -159,8 +162,12 @@ __device__ __forceinline__ int fine_bin<int64_t>(int64_t k, int shift, long long
     return (int)min((long long)__umul64hi((unsigned long long)d, fmul), (long long)(kSplitFine - 1));
 }
 
-// One CTA per candidate bucket: 32 sample loads per thread in flight, a
-// shared-memory fine-bin histogram, then the decision and the map.
+// One CTA per chunk of a candidate bucket (or per bucket when c > kMapChunksMax):
+// a 4k-key sample decides whether the range is skewed; a skewed one takes 32k
+// samples for its map.  Shared-memory fine-bin histogram, the chunk's map, and
+// the skew flag -- one skewed chunk puts its bucket in map mode (every chunk
+// then uses its own map: sorted or locally clustered inputs give each chunk a
+// different value range).
 template <typename K>
 __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__restrict__ S, uint16_t *map,
                                                            int tile_keys) {
@@ -170,53 +177,80 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
     __shared__ uint32_t h[kSplitFine + 1];  // fine-bin histogram, then its exclusive prefix (+ total)
     __shared__ uint32_t wsum[NT / 32];
     __shared__ unsigned s_max;
+    static_assert(SPT % 8 == 0, "phase-1 share");
     Plan &P = ctl->plan;
     SplitCfg &C = ctl->split;
-    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int mc = C.map_chunks;
+    const int b = blockIdx.x / mc, jj = blockIdx.x % mc, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (!C.cand[b] || C.fmul[b] == 0) return;
-    const long long m = P.off[b + 1] - P.off[b], base = P.off[b];
+    const long long mb = P.off[b + 1] - P.off[b];
+    long long base = P.off[b], m = mb;  // the sampled range: chunk jj, or the whole bucket
+    if (mc > 1) {
+        const long long c0 = part_start(mb, P.log2c, jj), c1 = part_start(mb, P.log2c, jj + 1);
+        base += c0;
+        m = c1 - c0;
+    }
+    if (m == 0) return;
     const long long lo = C.lo[b];
     const unsigned long long fmul = C.fmul[b];
     const int shift = C.shift;
-    const int ns = P.nsb[b];
-    for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
-    if (tid == 0) s_max = 0;
-    __syncthreads();
-    constexpr int R = 16;  // samples per round and thread (loads of a round in flight together)
-    static_assert(SPT % R == 0, "sample rounds");
+    const int ns = C.ns0[b];
+    // sample rank r in [0, kSplitSamples) -> position (r m) >> log2 (evenly spaced over the range).
+    // Phase 1 takes every 8th rank (4k samples): enough to tell a uniform range (the common case,
+    // stops here) from a skewed one; a skewed range takes the other 28k ranks for its map.
+    auto sample = [&](bool phase2) {
+        if (!phase2) {
+            constexpr int R1 = SPT / 8;
+            K kk[R1];
+#pragma unroll
+            for (int j = 0; j < R1; ++j) {
+                const unsigned long long r = 8ull * (unsigned long long)(j * NT + tid);  // < kSplitSamples
+                kk[j] = __ldg(S + base + (long long)((r * (unsigned long long)m) >> kSplitSamplesLog2));
+            }
+#pragma unroll
+            for (int j = 0; j < R1; ++j) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
+        } else {
+            constexpr int R = 8;  // loads per round and thread (in flight together)
 #pragma unroll 1
-    for (int j0 = 0; j0 < SPT; j0 += R) {
-        K kk[R];
+            for (int j0 = 0; j0 < SPT; j0 += R) {
+                K kk[R];
+                bool ok[R];
 #pragma unroll
-        for (int j = 0; j < R; ++j) {  // evenly spaced positions of the bucket
-            const unsigned long long r = (unsigned long long)((j0 + j) * NT + tid);
-            kk[j] = __ldg(S + base + (long long)((r * (unsigned long long)m) >> kSplitSamplesLog2));
+                for (int j = 0; j < R; ++j) {
+                    const unsigned long long r = (unsigned long long)((j0 + j) * NT + tid);  // < kSplitSamples
+                    ok[j] = (r & 7ull) != 0;  // the phase-1 ranks are already counted
+                    kk[j] = ok[j] ? __ldg(S + base + (long long)((r * (unsigned long long)m) >> kSplitSamplesLog2))
+                                  : K(0);
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if (ok[j]) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
+            }
         }
+    };
+    uint32_t hv[PER], excl0 = 0, total = 0;
+    // h holds a fine-bin histogram: hv <- my bins, total, excl0 <- my first bin's exclusive prefix,
+    // s_max <- the largest equal-width sub-range count; h ends as the exclusive prefix
+    auto analyze = [&]() {
+        uint32_t sum = 0;
 #pragma unroll
-        for (int j = 0; j < R; ++j) atomicAdd(&h[fine_bin<K>(kk[j], shift, lo, fmul)], 1u);
-    }
-    __syncthreads();
-    uint32_t hv[PER], sum = 0;
+        for (int j = 0; j < PER; ++j) {
+            hv[j] = h[tid * PER + j];
+            sum += hv[j];
+        }
+        if (tid == 0) s_max = 0;
+        uint32_t incl = sum;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        hv[j] = h[tid * PER + j];
-        sum += hv[j];
-    }
-    // block exclusive scan of the per-thread sums (its barrier also frees h for the estimates)
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    const uint32_t wl = lane < NT / 32 && lane < warp ? wsum[lane] : 0u;
-    const uint32_t excl0 = incl - sum + __reduce_add_sync(0xffffffffu, wl);
-    const uint32_t wt = lane < NT / 32 ? wsum[lane] : 0u;
-    const uint32_t total = __reduce_add_sync(0xffffffffu, wt);
-    // h <- exclusive prefix of the fine bins (everyone read its hv before the scan's barrier)
-    {
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        const uint32_t wl = lane < NT / 32 && lane < warp ? wsum[lane] : 0u;
+        excl0 = incl - sum + __reduce_add_sync(0xffffffffu, wl);
+        const uint32_t wt = lane < NT / 32 ? wsum[lane] : 0u;
+        total = __reduce_add_sync(0xffffffffu, wt);
         uint32_t run0 = excl0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -224,11 +258,9 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
             run0 += hv[j];
         }
         if (tid == 0) h[kSplitFine] = total;
-    }
-    __syncthreads();
-    // equal-width sub-range t holds (about) the fine bins i with floor(i ns / kSplitFine) = t,
-    // i.e. [ceil(t F / ns), ceil((t+1) F / ns)): its sample count is a prefix difference
-    {
+        __syncthreads();
+        // equal-width sub-range t holds (about) the fine bins i with floor(i ns / kSplitFine) = t,
+        // i.e. [ceil(t F / ns), ceil((t+1) F / ns)): its sample count is a prefix difference
         uint32_t mx = 0;
         for (int t = tid; t < ns; t += NT) {
             const int lo_i = (t * kSplitFine + ns - 1) / ns, hi_i = ((t + 1) * kSplitFine + ns - 1) / ns;
@@ -237,27 +269,54 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
         }
         mx = __reduce_max_sync(0xffffffffu, mx);
         if (lane == 0) atomicMax(&s_max, mx);
-    }
+        __syncthreads();
+    };
+    // skewed: the largest sample count is beyond the sampling noise of a uniform range,
+    // > mean + 5 sqrt(mean) + 1 (mean = total / ns; the max of ns Poisson counts stays
+    // within ~3.5 sqrt(mean) of it)
+    auto is_skewed = [&]() {
+        const float mean_s = (float)total / (float)ns;
+        return total > 0 && (float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f;
+    };
+    for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
     __syncthreads();
-    // keep equal width unless the largest sample count is beyond the sampling noise of a
-    // uniform bucket: > mean + 5 sqrt(mean) + 1 (mean = total / ns samples per sub-range;
-    // the max of ns Poisson counts stays within ~3.5 sqrt(mean) of it)
-    const float mean_s = (float)total / (float)ns;
-    const bool skewed = total > 0 && (float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f;
-    if (!skewed) return;  // mode stays 0
-    const long long c = 1LL << P.log2c, cm = (m + c - 1) / c;
+    sample(false);
+    __syncthreads();
+    analyze();
+    bool skewed = is_skewed();
+    if (skewed) {  // uniform per CTA: the full sample for the map
+        uint32_t h1[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) h1[j] = hv[j];
+        for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
+        __syncthreads();
+        sample(true);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) h[tid * PER + j] += h1[j];  // my own bins: no race
+        __syncthreads();
+        analyze();
+        skewed = is_skewed();
+    }
+    if (!skewed && mc == 1) return;  // a bucket-wide map is only needed when skewed
+    const long long c = 1LL << P.log2c, cm = (mb + c - 1) / c;
     const long long tm = split_target_map(tile_keys);
     long long ns2 = (cm + tm - 1) / tm;
     if (ns2 > C.nsa[b]) ns2 = C.nsa[b];
     if (ns2 < 2) ns2 = 2;
+    // every chunk writes its map (another chunk of the bucket may be the skewed one): equal-count
+    // groups of its sample -- unless the chunk looked uniform and its 4k sample is too thin for
+    // ns2 groups (< 64 samples each), then equal-width groups of fine bins
+    uint16_t *const cmap = map + ((size_t)b * mc + jj) * kSplitFine;
+    const bool by_count = skewed || total >= 64u * (unsigned)ns2;
     uint32_t run = excl0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const long long g = (long long)run * ns2 / total;
-        map[b * kSplitFine + tid * PER + j] = (uint16_t)(g < ns2 - 1 ? g : ns2 - 1);
+        const long long g = by_count ? (long long)run * ns2 / total : (long long)(tid * PER + j) * ns2 / kSplitFine;
+        cmap[tid * PER + j] = (uint16_t)(g < ns2 - 1 ? g : ns2 - 1);
         run += hv[j];
     }
-    if (tid == 0) {
+    if (skewed && tid == 0) {  // idempotent: every skewed chunk of the bucket writes the same values
         P.nsb[b] = (int)ns2;
         C.mode[b] = 1;
     }
@@ -341,7 +400,7 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
     sd.lo = C.lo[b];
     sd.mul = C.mul[b];
     sd.fmul = C.fmul[b];
-    sd.bmap = C.mode[b] ? map + b * kSplitFine : nullptr;
+    sd.bmap = C.mode[b] ? map + ((size_t)b * C.map_chunks + (C.map_chunks > 1 ? j : 0)) * kSplitFine : nullptr;
     sd.shift = C.shift;
 }
 
@@ -595,10 +654,13 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
 
 // ------------------------------------------------------------------ host
 // words after the split table: fine histograms (u32) and sampled maps (u16) of the 10 buckets
-constexpr long long kSplitExtraWords = 10LL * kSplitFine / 2;
+static long long split_extra_words(int log2c) {  // the sampled maps (u16) after the split table
+    const long long mc = (1LL << log2c) <= kMapChunksMax ? (1LL << log2c) : 1;
+    return 10LL * mc * kSplitFine / 2;
+}
 
 long long split_table_words(long long n, int log2c, int tile_keys) {
-    return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + kSplitExtraWords;
+    return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + split_extra_words(log2c);
 }
 
 static int nsb_bound(long long n, int log2c, int tile_keys) {
@@ -629,13 +691,15 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long c = 1LL << log2c;
     const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
-    const long long tab_cap = tab_words - kSplitExtraWords;
+    const long long tab_cap = tab_words - split_extra_words(log2c);
     uint16_t *const map = reinterpret_cast<uint16_t *>(tab + tab_cap);
     prof_begin(kProfPlan, st);
     if ((e = launch_pdl(k_split_setup, dim3(1), dim3(1024), 0, st, ctl, div, 8 * (int)sizeof(K), key_shift,
                         tile_keys, TS, tab_cap, nsb_cap, tab)) != cudaSuccess)
         return e;
-    if ((e = launch_pdl(k_split_sample_map<K>, dim3(10), dim3(1024), 0, st, ctl, S, map, tile_keys)) != cudaSuccess)
+    const int mc = (1LL << log2c) <= kMapChunksMax ? (int)(1LL << log2c) : 1;
+    if ((e = launch_pdl(k_split_sample_map<K>, dim3(10 * mc), dim3(1024), 0, st, ctl, S, map, tile_keys)) !=
+        cudaSuccess)
         return e;
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);

@@ -125,11 +125,27 @@ def test_split_clamped_and_negative_inside_split_buckets():
 
 
 def test_split_sorted_and_reversed_input():
+    """Sorted input: every chunk covers its own slice of the bucket's value range, so equal-width
+    sub-ranges of the bucket overflow; the per-chunk sampled maps split every chunk anyway."""
     t = T(0)
     n = 10 * 2 * 3 * t
     for keys in (np.arange(n, dtype=np.int32) * 13, (np.arange(n, dtype=np.int32) * 13)[::-1].copy()):
         D = len(str(int(keys.max())))
-        check(keys, D, 2)
+        plan = check(keys, D, 2)
+        off = np.concatenate([[0], np.cumsum(np.bincount(np.minimum(keys // 10 ** (D - 1), 9), minlength=10))])
+        for b in range(10):
+            if off[b + 1] - off[b] > 2 * t:     # chunks larger than a tile
+                assert plan["split"][b] == 1, (b, plan)
+
+
+def test_split_sorted_runs_c8():
+    """Nearly sorted data with c = 8 (per-chunk maps for every chunk of a large bucket)."""
+    t = T(0)
+    rng = np.random.default_rng(91)
+    n = 8 * 4 * t * 3
+    keys = (np.sort(rng.integers(0, 3 * 10**7, size=n)) + rng.integers(0, 50, size=n)).astype(np.int32)
+    plan = check(keys, 8, 8)
+    assert plan["split"][0] == 1 and plan["split"][1] == 1 and plan["split"][2] == 1
 
 
 def test_split_duplicates_half_the_keys():
@@ -242,3 +258,21 @@ def test_sort_buckets_misaligned_and_empty():
     assert np.array_equal(got[1:-1], np.sort(keys))
     e = torch.empty(0, dtype=torch.int32, device=DEV)
     hs.hs_sort_buckets(e, torch.zeros(11, dtype=torch.int64, device=DEV), 8, 8)
+
+
+def test_split_half_sorted_bucket():
+    """Chunks 0-3 of each bucket sorted, chunks 4-7 random: the sorted chunks put the bucket in map
+    mode, the random ones use equal-width groups of fine bins."""
+    t = T(0)
+    rng = np.random.default_rng(93)
+    D, c = 9, 8
+    div = 10 ** (D - 1)
+    parts = []
+    for b in range(10):
+        m = c * 3 * t
+        half = np.sort(rng.integers(b * div, (b + 1) * div, size=m // 2))
+        rest = rng.integers(b * div, (b + 1) * div, size=m - m // 2)
+        parts.append(np.concatenate([half, rest]))
+    keys = np.concatenate(parts).astype(np.int32)   # already bucket-major: the stable partition keeps it
+    plan = check(keys, D, c)
+    assert sum(plan["split"]) >= 8

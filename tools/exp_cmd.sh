@@ -1,3 +1,2 @@
-mkdir -p gpurun_out/e8
-python tools/exp.py run main pdl > gpurun_out/e8/exp.log 2>&1
-python tools/exp.py run main pdl >> gpurun_out/e8/exp.log 2>&1
+mkdir -p gpurun_out/e10
+python tools/exp.py run main s64v16 --cfg C5 > gpurun_out/e10/exp.log 2>&1
