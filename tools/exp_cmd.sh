@@ -1,2 +1,3 @@
-mkdir -p gpurun_out/e10
-python tools/exp.py run main s64v16 --cfg C5 > gpurun_out/e10/exp.log 2>&1
+mkdir -p gpurun_out/e11
+python tools/exp.py run main k3sd > gpurun_out/e11/exp.log 2>&1
+python tools/exp.py run main k3sd --cfg C5 >> gpurun_out/e11/exp.log 2>&1
