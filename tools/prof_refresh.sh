@@ -1,6 +1,6 @@
 # Round profile refresh: bench line, launch list, ncu full capture (second call of one_call.py)
 set -x
-OUT=gpurun_out/p5
+OUT=gpurun_out/p6
 mkdir -p $OUT
 python bench.py > $OUT/bench.json 2> $OUT/bench.log || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
