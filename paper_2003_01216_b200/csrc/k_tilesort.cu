@@ -52,13 +52,13 @@
 #define HS_SORT_CAP 48  // keys per bucket sorted in registers (mean T / 2NT = 26.5)
 #endif
 #ifndef HS_SORT_BUCKETS64
-#define HS_SORT_BUCKETS64 4  // int64: buckets per thread (16-bit packed counters)
+#define HS_SORT_BUCKETS64 2  // int64: buckets per thread (16-bit packed counters)
 #endif
 #ifndef HS_SORT_BUNROLL
 #define HS_SORT_BUNROLL 1
 #endif
 #ifndef HS_SORT_CAP64
-#define HS_SORT_CAP64 20  // mean T / 4NT = 6.75
+#define HS_SORT_CAP64 28  // mean 0.9 T / 2NT = 12 on split leaves (1024 buckets): few tiles overflow
 #endif
 
 namespace hs {
