@@ -276,3 +276,17 @@ def test_split_half_sorted_bucket():
     keys = np.concatenate(parts).astype(np.int32)   # already bucket-major: the stable partition keeps it
     plan = check(keys, D, c)
     assert sum(plan["split"]) >= 8
+
+
+def test_split_many_chunks_bucket_map():
+    """c = 128 > kMapChunksMax: one sampled map per bucket (not per chunk); a skewed bucket still splits."""
+    t, D, c = T(0), 9, 128
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(97)
+    m = c * 2 * t
+    peak = np.clip(rng.normal(3.4 * div, div / 30, size=m), 3 * div, 4 * div - 1).astype(np.int64)
+    other = rng.integers(0, 10 * div, size=200_000)
+    keys = np.concatenate([peak, other]).astype(np.int32)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert plan["split"][3] == 1 and plan["levels"][3] == 7
