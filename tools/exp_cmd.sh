@@ -1,2 +1,3 @@
-mkdir -p gpurun_out/e13
-python tools/exp.py run main t64b2c28 t64b2c30 --cfg C5 > gpurun_out/e13/exp.log 2>&1
+mkdir -p gpurun_out/e14
+python tools/exp.py run cp1 cp2 cp4 > gpurun_out/e14/exp.log 2>&1
+python tools/exp.py run cp1 cp2 cp4 >> gpurun_out/e14/exp.log 2>&1
