@@ -87,34 +87,53 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
                               int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ long long s_words;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // lane b < 10: bucket b's geometry (64-bit divisions in parallel)
         Plan &P = ctl->plan;
         SplitCfg &C = ctl->split;
+        const int b = threadIdx.x;
         const long long c = 1LL << P.log2c, target = split_target(tile_keys);
         const long long target_m = split_target_map(tile_keys);
         const unsigned long long wmax = key_bits == 32 ? 0xFFFFFFFFull : ~0ull;
-        long long acc_s = 0, acc_t = 0;
-        for (int b = 0; b < 10; ++b) {
+        long long ns = 0, nsa = 0, spc = 0;
+        bool cand = false;
+        if (b < 10) {
             const long long m = P.off[b + 1] - P.off[b], cm = (m + c - 1) / c;
-            const long long ns = (cm + target - 1) / target;
-            long long nsa = (cm + target_m - 1) / target_m;
+            ns = (cm + target - 1) / target;
+            nsa = (cm + target_m - 1) / target_m;
             if (nsa > nsb_cap) nsa = nsb_cap;
             if (nsa < ns) nsa = ns;
+            spc = (cm + slice_keys - 1) / slice_keys;
             // ns <= div: the multiplier below fits the key width (and narrower sub-ranges would be empty)
-            const bool cand = P.k[b] > 0 && ns >= 2 && ns <= nsb_cap && (unsigned long long)ns <= div &&
-                              acc_t + c * (nsa + 1) <= tab_cap;
-            C.cand[b] = cand;
+            cand = P.k[b] > 0 && ns >= 2 && ns <= nsb_cap && (unsigned long long)ns <= div;
+        }
+        // table capacity check and prefixes, in bucket order (lane 0, ten steps)
+        long long words = cand ? c * (nsa + 1) : 0;
+        long long ac_t = 0, ac_s = 0, acc_t = 0, acc_s = 0;
+        bool ok = cand;
+        for (int q = 0; q < 10; ++q) {
+            const long long wq = __shfl_sync(0xffffffffu, words, q);
+            const long long sq = __shfl_sync(0xffffffffu, cand ? c * spc : 0LL, q);
+            const bool cq = __shfl_sync(0xffffffffu, cand ? 1 : 0, q) && acc_t + wq <= tab_cap;
+            if (q == b) {
+                ok = cq;
+                ac_t = acc_t;
+                ac_s = acc_s;
+            }
+            if (cq) {
+                acc_t += wq;
+                acc_s += sq;
+            }
+        }
+        if (b < 10) {
+            C.cand[b] = ok;
             C.mode[b] = 0;
-            C.slice_prefix[b] = acc_s;
-            if (cand) {
-                const long long spc = (cm + slice_keys - 1) / slice_keys;
+            C.slice_prefix[b] = ac_s;
+            if (ok) {
                 C.spc[b] = (int)spc;
-                acc_s += c * spc;
                 P.nsb[b] = (int)ns;
                 C.ns0[b] = (int)ns;
                 C.nsa[b] = (int)nsa;
-                P.sboff[b] = acc_t;
-                acc_t += c * (nsa + 1);
+                P.sboff[b] = ac_t;
                 C.lo[b] = (long long)b * (long long)div;
                 C.mul[b] = wmax / div * (unsigned long long)ns;  // <= wmax since ns <= div
                 // fine bins for the sampled map (needs >= 1 value per fine bin; nsa <= kSplitFine)
@@ -128,10 +147,12 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
                 C.nsa[b] = 0;
             }
         }
-        C.slice_prefix[10] = acc_s;
-        C.shift = key_shift;
-        C.map_chunks = c <= kMapChunksMax ? (int)c : 1;
-        s_words = acc_t;
+        if (b == 0) {
+            C.slice_prefix[10] = acc_s;
+            C.shift = key_shift;
+            C.map_chunks = c <= kMapChunksMax ? (int)c : 1;
+            s_words = acc_t;
+        }
     }
     __syncthreads();
     for (long long q = threadIdx.x; q < s_words; q += blockDim.x) tab[q] = 0;
