@@ -1,4 +1,2 @@
-mkdir -p gpurun_out/e15
-python tools/exp.py run main mpw0 mpw > gpurun_out/e15/exp.log 2>&1
-python tools/exp.py run main mpw0 mpw >> gpurun_out/e15/exp.log 2>&1
-python tools/exp.py run main mpw --cfg C5 >> gpurun_out/e15/exp.log 2>&1
+mkdir -p gpurun_out/e17
+python tools/exp.py run main m256 m256v21 m192v33 m128v49 > gpurun_out/e17/exp.log 2>&1
