@@ -1,4 +1,5 @@
-// k_split.cu -- K5a: value split of each chunk before its tile sort (hs_sort).
+// k_split.cu -- K5a: value split of each chunk before its tile sort
+// (hs_sort, hs_sort_buckets, hs_sort_pairs).
 //
 // a5 sorts every chunk of every bucket ("sort the partitions",
 // the paper's per-thread quicksort).  A chunk of C3 holds 3.4M keys, far more
@@ -12,27 +13,29 @@
 // sub-ranges, laid end to end, ARE the sorted chunk.  What remains of K6 is
 // the paper's binary tree merge of the c sorted chunks (a6).
 //
-//   k_split_setup    1 CTA: per-bucket sub-range count, slice counts, table
-//                    offsets; zeroes the count table
-//   k_split_sample_map  one CTA per chunk of a candidate bucket: fine-bin
-//                    histogram of a 32k-key sample of the chunk and its equal-
-//                    count map; the bucket keeps equal-width sub-ranges unless
-//                    some chunk's largest sample count is beyond the sampling
-//                    noise of a uniform range (then every chunk uses its map)
-//   k_split_count    persistent CTAs read slices (<= NT*VT keys of one chunk)
-//                    of S, count their sub-ranges in shared memory and add the
-//                    non-zero counts to the chunk's table row (next slice's
-//                    loads in flight during the flush)
-//   k_split_plan     one CTA per chunk: exclusive scan of the row -> sub-range
-//                    starts (+ cursor copy); a sub-range over T keys marks the
-//                    bucket "bad"; the last CTA finalises the Plan: split
-//                    buckets get k = 0, L = log2 c, leaves = sub-ranges; bad
-//                    buckets keep the tile + in-chunk merge plan (skewed keys,
-//                    heavy duplicates: correct either way, only slower)
-//   k_split_scatter  one CTA per slice: counted again, every non-empty
-//                    sub-range claims its output span with one global atomic,
-//                    the keys are staged by sub-range in shared memory and
-//                    written out run by run (coalesced within a sub-range)
+//   k_split_setup       1 CTA: per-bucket sub-range counts, slices, table
+//                       offsets (ten lanes in parallel); zeroes the table
+//   k_split_sample_map  one CTA per chunk of a candidate bucket (per bucket
+//                       beyond kMapChunksMax chunks): a 4k-key sample over
+//                       8192 fine equal-width bins; a chunk that looks skewed
+//                       takes 32k samples and writes its equal-count map, and
+//                       puts its bucket in map mode
+//   k_split_count       persistent CTAs over slices (<= NT*VT keys of one
+//                       chunk) of the partitioned keys: shared-memory histogram
+//                       of the sub-ranges, non-zero counts added to the chunk's
+//                       table row (next slice's loads in flight during the flush)
+//   k_split_plan        one CTA per chunk: exclusive scan of the row -> sub-range
+//                       starts (+ cursor copy); a sub-range over T keys marks
+//                       the bucket "bad"; the last CTA finalises the Plan: split
+//                       buckets get k = 0, L = log2 c, leaves = sub-ranges; bad
+//                       buckets keep the tile + in-chunk merge plan (a value
+//                       with more than a tile of copies in a chunk: correct
+//                       either way, only slower)
+//   k_split_scatter     persistent CTAs over the same slices: ranks by shared
+//                       atomics, one global atomic per non-empty sub-range
+//                       claims the slice's output span, (destination, key)
+//                       staged in shared memory and written run by run
+//                       (coalesced within a sub-range)
 //
 // The order of keys inside a sub-range depends on atomic arrival order; the
 // tile sort that follows makes the result the unique sorted chunk (keys only;
@@ -40,9 +43,8 @@
 // Sub-range of a key: min(mulhi(max(x - lo_b, 0), mul), nsb - 1) with mul =
 // floor((2^w - 1) / 10^(D-1)) nsb -- non-decreasing in the key, so sub-range
 // order is key order; keys clamped into bucket 0 / 9 (P:78 reading #3) land in
-// the first / last sub-range.  Skewed buckets (k_split_sample_map)
-// use equal-count groups of 8192 fine equal-width bins instead, picked from a
-// 32k-key sample: map[fine bin] is non-decreasing, so the order argument holds.
+// the first / last sub-range.  In map mode the sub-range is map[fine bin], and
+// every map is non-decreasing in the fine bin, so the order argument holds.
 // Roofline: HBM, 4 B read (count) + 8 B read+write (scatter) per int32 key.
 #include <cstdint>
 
