@@ -78,7 +78,14 @@ struct SplGeo<int64_t> {
 constexpr int kSplitMaxSub = 4096;  // sub-ranges per chunk (shared-memory counters)
 constexpr int kSplitPlanNT = 512;
 
-__host__ __device__ __forceinline__ long long split_target(int tile_keys) { return (long long)tile_keys * 9 / 10; }
+#ifndef HS_SPLIT_TARGET_PCT
+#define HS_SPLIT_TARGET_PCT 90
+#endif
+// equal-width sub-ranges aim at this share of a tile (uniform keys: the largest of ~10^4
+// sub-ranges stays a few standard deviations, ~1%, above the mean)
+__host__ __device__ __forceinline__ long long split_target(int tile_keys) {
+    return (long long)tile_keys * HS_SPLIT_TARGET_PCT / 100;
+}
 
 // ------------------------------------------------------------------ setup
 // Row capacity per chunk for a sampled (skewed) bucket: sub-ranges of ~0.7 T

@@ -1,2 +1,4 @@
-mkdir -p gpurun_out/e17
-python tools/exp.py run main m256 m256v21 m192v33 m128v49 > gpurun_out/e17/exp.log 2>&1
+mkdir -p gpurun_out/e18
+python tools/exp.py run main tg93 tg96 > gpurun_out/e18/exp.log 2>&1
+python tools/exp.py run main tg93 tg96 --cfg C5 >> gpurun_out/e18/exp.log 2>&1
+python tools/exp.py run main tg93 tg96 --cfg C2 >> gpurun_out/e18/exp.log 2>&1
