@@ -304,9 +304,20 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
     // skewed: the largest sample count is beyond the sampling noise of a uniform range,
     // > mean + 5 sqrt(mean) + 1 (mean = total / ns; the max of ns Poisson counts stays
     // within ~3.5 sqrt(mean) of it)
+    // A smooth density change (a ramp) is too gentle for the per-sub-range test at 4k samples,
+    // but 8 coarse groups of the range average the noise away: a group beyond mean + 5 sqrt(mean)
+    // (~1.22x at 4k samples) means equal-width sub-ranges of ~0.9 T would overflow somewhere.
     auto is_skewed = [&]() {
         const float mean_s = (float)total / (float)ns;
-        return total > 0 && (float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f;
+        uint32_t cmax = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const uint32_t e = h[(g + 1) * (kSplitFine / 8)] - h[g * (kSplitFine / 8)];  // h: the prefix
+            cmax = e > cmax ? e : cmax;
+        }
+        const float mean_c = (float)total / 8.0f;
+        return total > 0 && ((float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f ||
+                             (float)cmax > mean_c + 5.0f * sqrtf(mean_c) + 1.0f);
     };
     for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
     __syncthreads();

@@ -290,3 +290,21 @@ def test_split_many_chunks_bucket_map():
     rng.shuffle(keys)
     plan = check(keys, D, c)
     assert plan["split"][3] == 1 and plan["levels"][3] == 7
+
+
+def test_split_density_ramp():
+    """Keys with a 1:3 linear density ramp inside every bucket: equal-width sub-ranges of 0.9 T would
+    overflow at the dense end (~1.35 x the mean); the coarse skew test sends the buckets to the map."""
+    t, D, c = T(0), 9, 8
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(101)
+    m = c * 3 * t
+    parts = []
+    for b in range(10):
+        u = rng.random(m)
+        x = (np.sqrt(u * 8 + 1) - 1) / 2          # density rising linearly from 1 to 3 over [0, 1)
+        parts.append(b * div + np.minimum((x * div).astype(np.int64), div - 1))
+    keys = np.concatenate(parts).astype(np.int32)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert sum(plan["split"]) == 10, plan

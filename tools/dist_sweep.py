@@ -19,6 +19,9 @@ cases = {
     "1000 distinct values": lambda: uni(0, 1000, n) * 999_983,
     "exponential (scale 5e7)": lambda: (torch.empty(n, device="cuda").exponential_(generator=g) * 5e7).clamp(0, 10**9 - 1).long(),
     "all equal": lambda: torch.full((n,), 123_456_789, device="cuda", dtype=torch.int64),
+    "linear ramp 1:3 per bucket": lambda: (torch.div(uni(0, 10**9, n), 10**8, rounding_mode="floor") * 10**8
+                                           + (torch.sqrt(torch.rand(n, device="cuda", generator=g) * 8 + 1) - 1)
+                                           .mul(10**8 / 2).long().clamp(0, 10**8 - 1)),
     "sorted runs of 2^16": lambda: torch.sort(uni(0, 10**9, n).view(-1, 1 << 16), dim=1).values.reshape(-1),
 }
 for name, make in cases.items():
