@@ -284,6 +284,10 @@ int hs_plan_levels(const int64_t *bucket_offsets_host, hs_dtype_t dtype, int chu
  *   bucket_offsets[11] in: device int64 CSR offsets, [0] = 0, [10] = n,
  *                      non-decreasing; NOT checked (it lives on the device).
  *   chunks_per_bucket  c, power of two in [1, 65536].
+ * Errors: HS_ERR_INVALID_VALUE (NULL or misaligned pointer, bad D or c),
+ * HS_ERR_UNSUPPORTED_DTYPE, HS_ERR_OUT_OF_MEMORY (scratch), HS_ERR_CUDA (a
+ * launch failed); detail in hs_last_error_message().  Enqueued on stream; no
+ * host synchronisation; scratch from the stream-ordered pool.
  */
 hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, const int64_t *bucket_offsets,
                             int chunks_per_bucket, cudaStream_t stream);
