@@ -1,2 +1,3 @@
-mkdir -p gpurun_out/e19
-python tools/dist_sweep.py > gpurun_out/e19/sweep.log 2>&1
+mkdir -p gpurun_out/e20
+python tools/exp.py run main k3n256 > gpurun_out/e20/exp.log 2>&1
+python tools/exp.py run main k3n256 --cfg C5 >> gpurun_out/e20/exp.log 2>&1
