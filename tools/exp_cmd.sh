@@ -1,3 +1,4 @@
-mkdir -p gpurun_out/e20
-python tools/exp.py run main k3n256 > gpurun_out/e20/exp.log 2>&1
-python tools/exp.py run main k3n256 --cfg C5 >> gpurun_out/e20/exp.log 2>&1
+mkdir -p gpurun_out/e21
+python tools/exp.py run main tsx > gpurun_out/e21/exp.log 2>&1
+python tools/exp.py run main tsx >> gpurun_out/e21/exp.log 2>&1
+python tools/exp.py run main tsx --cfg C2 >> gpurun_out/e21/exp.log 2>&1
