@@ -1,3 +1,5 @@
-mkdir -p gpurun_out/s38
-timeout 600 python -m pytest tests/test_next_rows.py tests/test_split.py -x -q -k "pairs" > gpurun_out/s38/tests.log 2>&1; echo "rc=$?" >> gpurun_out/s38/tests.log
-timeout 300 python bench.py --api pairs --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s38/b_pairs.json 2> gpurun_out/s38/b_pairs.log
+mkdir -p gpurun_out/final2
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/final2/tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/final2/tests.log
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/final2/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final2/smoke.log
+python bench.py > gpurun_out/final2/bench.json 2> gpurun_out/final2/bench.log
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final2/ref.json 2> gpurun_out/final2/ref.log
