@@ -116,7 +116,28 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def run_reference(args, cfg):
+    """The base contract's reference arm, which for this paper is the CPU oracle (oracle/,
+    plain C; its OpenMP build runs the paper's own shared-memory scheme on the box's host
+    cores: chunks, then merge pairs, in parallel), timed as it stands on bounded samples."""
     import oracle
     import workload as W
     sample = min(cfg.n, args.ref_sample)
@@ -126,7 +147,7 @@ def run_reference(args, cfg):
     for i in range(nsteps):
         start = (i * sample) % max(cfg.n - sample + 1, 1)
         keys = W.generate(cfg, start, sample)
-        _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
+        _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks, openmp=True)
         if i >= args.warmup:
             times.append(dt)
     sec = statistics.mean(times)
@@ -137,29 +158,50 @@ def run_reference(args, cfg):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "sample_keys_per_step": sample,
-                   "parallelism": "single host thread (plain oracle)"},
+                   "parallelism": f"host CPU, OpenMP oracle on {threads} threads ({cpu_model()})"},
         "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": threads, "kind": "oracle",
+                         "cpu": cpu_model(),
                          "sample": f"{sample:,} consecutive keys of {cfg.name} per step (bounded sample), "
-                                   "plain single-thread C oracle (gcc -O2), time of the sort call only"},
+                                   "OpenMP build of the plain C oracle (gcc -O2 -fopenmp; chunk quicksorts and "
+                                   "merge pairs in parallel, P:58-62), time of the sort call only"},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------- ours
-def cpu_baseline(cfg, sample, shared=False):
+def cpu_baseline(cfg, sample, shared=False, sample_omp=None):
+    """The oracle timed on this host, as it stands: its OpenMP build (the paper's shared-memory
+    scheme on all host cores) on sample_omp keys -- the reported value -- and the plain
+    single-thread build on `sample` keys beside it."""
     import oracle
     import workload as W
-    keys = W.generate(cfg, 0, sample)
-    if shared:
-        t0 = time.perf_counter()
-        oracle.sort_shared(keys, cfg.chunks)
-        dt, threads = time.perf_counter() - t0, 1
-    else:
-        _, dt, threads = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks)
-    return {"value": sample / dt / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {sample:,} keys of {cfg.name} ({sample / cfg.n:.3g} of the workload), plain "
-                      f"single-thread C oracle (gcc -O2), {dt:.2f} s for the sort call only"}
+    ncores = host_cores()
+
+    def one(nkeys, openmp):
+        keys = W.generate(cfg, 0, nkeys)
+        if shared:
+            t0 = time.perf_counter()
+            oracle.sort_shared(keys, cfg.chunks, openmp=openmp)
+            dt = time.perf_counter() - t0
+            thr = ncores if openmp else 1
+        else:
+            _, dt, thr = oracle.timed_sort(keys, cfg.num_digits, cfg.chunks, openmp=openmp)
+        return nkeys / dt / 1e9, dt, thr
+
+    n1 = sample
+    v1, t1, _ = one(n1, False)
+    single = {"value": v1, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+              "sample": f"first {n1:,} keys of {cfg.name} ({n1 / cfg.n:.3g} of the workload), plain single-thread "
+                        f"C oracle (gcc -O2), {t1:.2f} s for the sort call only"}
+    no = min(cfg.n, sample_omp or cfg.n)
+    vo, to, thr = one(no, True)
+    return {"value": vo, "unit": "Gkeys/s", "cores": thr, "kind": "oracle", "cpu": cpu_model(),
+            "host_cores": ncores,
+            "sample": f"first {no:,} keys of {cfg.name} ({no / cfg.n:.3g} of the workload), OpenMP build of the "
+                      f"plain C oracle (gcc -O2 -fopenmp, {thr} threads: chunk quicksorts, then merge pairs, in "
+                      f"parallel -- the paper's shared-memory scheme, P:58-62), {to:.2f} s for the sort call only",
+            "single_core": single}
 
 
 def run_ours(args, cfg):
@@ -376,7 +418,7 @@ def run_ours(args, cfg):
                 f"{d.get('alg_GBps', 0):7.0f} GB/s alg")
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg, min(cfg.n, args.cpu_sample), shared)
+            cpu = cpu_baseline(cfg, min(cfg.n, args.cpu_sample), shared, args.cpu_sample_omp)
             log(f"[bench] cpu_baseline {cpu}")
         line = {
             "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
@@ -486,7 +528,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=1 << 26)
-    ap.add_argument("--ref-sample", type=int, default=1 << 23)
+    ap.add_argument("--cpu-sample-omp", type=int, default=0, help="keys for the OpenMP oracle (0: the whole workload)")
+    ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")

@@ -141,8 +141,9 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
  * sampled key distribution is skewed, equal-count groups of 2048 fine bins),
  * each of which is then sorted in one shared-memory tile; a bucket whose
  * sub-ranges still overflow a tile (a value with more than a tile of copies in
- * a chunk) falls back to tile sort + in-chunk merge levels.  Either way the result is the unique ascending array.  The split
- * is on unless the environment variable HS_SPLIT=0 is set (A/B measurements).
+ * a chunk) falls back to tile sort + in-chunk merge levels.  Either way the
+ * result is the unique ascending array.  (A build with -DHS_SPLIT=0 omits the
+ * split, for A/B measurements only; nothing at run time changes the path.)
  *
  *   keys[n]            in/out: device; ascending on return.
  *   num_digits, chunks_per_bucket: as above.

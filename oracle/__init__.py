@@ -158,19 +158,19 @@ def merge_runs(left, right) -> np.ndarray:
     return out
 
 
-def sort_chunks(x, offsets, chunks: int) -> np.ndarray:
+def sort_chunks(x, offsets, chunks: int, openmp: bool = False) -> np.ndarray:
     src = np.asarray(x)
     k = _w(src)
     off = _w(offsets)
-    _check(_lib().oracle_sort_chunks(_p(k), _p(k), k.size, _p(off), chunks))
+    _check(_lib(openmp).oracle_sort_chunks(_p(k), _p(k), k.size, _p(off), chunks))
     return k.astype(src.dtype)
 
 
-def merge(x, offsets, chunks: int) -> np.ndarray:
+def merge(x, offsets, chunks: int, openmp: bool = False) -> np.ndarray:
     src = np.asarray(x)
     k = _w(src)
     off = _w(offsets)
-    _check(_lib().oracle_merge(_p(k), _p(k), k.size, _p(off), chunks))
+    _check(_lib(openmp).oracle_merge(_p(k), _p(k), k.size, _p(off), chunks))
     return k.astype(src.dtype)
 
 

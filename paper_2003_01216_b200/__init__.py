@@ -214,27 +214,37 @@ def hs_msd_partition(keys, num_digits: int, out=None, bucket_offsets=None, strea
         bucket_offsets = torch.empty(11, dtype=torch.int64, device=keys.device)
     _check_tensor(out, "out")
     _check_tensor(bucket_offsets, "bucket_offsets")
-    if out.dtype != keys.dtype or out.numel() != keys.numel():
-        raise ValueError("out must match keys in dtype and size")
-    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
-        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    if out.dtype != keys.dtype or out.numel() != keys.numel() or out.device != keys.device:
+        raise ValueError("out must match keys in dtype, size and device")
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11 or bucket_offsets.device != keys.device:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements on the keys' device")
     with torch.cuda.device(keys.device):
         _check(load().hs_msd_partition(keys.data_ptr(), keys.numel(), dt, num_digits, bucket_offsets.data_ptr(),
                                        out.data_ptr(), _stream(stream)))
     return out, bucket_offsets
 
 
+def _check_out(x, out, bucket_offsets) -> None:
+    """out must match x in dtype, size and device (the library writes n * itemsize bytes
+    into it); bucket_offsets must be int64[11] on x's device (the kernels read it)."""
+    torch = _torch()
+    _check_tensor(out, "out")
+    _check_tensor(bucket_offsets, "bucket_offsets")
+    if out.dtype != x.dtype or out.numel() != x.numel() or out.device != x.device:
+        raise ValueError(f"out must match x in dtype, size and device: got {out.dtype}[{out.numel()}] on "
+                         f"{out.device} for {x.dtype}[{x.numel()}] on {x.device}")
+    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11 or bucket_offsets.device != x.device:
+        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements on x's device")
+
+
 def hs_sort_chunks(x, bucket_offsets, chunks_per_bucket: int = 8, out=None, stream=None):
     """Sort every chunk of every bucket.  out=x sorts in place."""
     torch = _torch()
     _check_tensor(x, "x")
-    _check_tensor(bucket_offsets, "bucket_offsets")
     dt = _dtype_code(x)
     if out is None:
         out = torch.empty_like(x)
-    _check_tensor(out, "out")
-    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
-        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    _check_out(x, out, bucket_offsets)
     with torch.cuda.device(x.device):
         _check(load().hs_sort_chunks(x.data_ptr(), out.data_ptr(), x.numel(), dt, bucket_offsets.data_ptr(),
                                      chunks_per_bucket, _stream(stream)))
@@ -245,13 +255,10 @@ def hs_merge(x, bucket_offsets, chunks_per_bucket: int = 8, out=None, stream=Non
     """Binary-tree merge of each bucket's sorted chunks.  out=x merges in place."""
     torch = _torch()
     _check_tensor(x, "x")
-    _check_tensor(bucket_offsets, "bucket_offsets")
     dt = _dtype_code(x)
     if out is None:
         out = torch.empty_like(x)
-    _check_tensor(out, "out")
-    if bucket_offsets.dtype != torch.int64 or bucket_offsets.numel() != 11:
-        raise ValueError("bucket_offsets must be an int64 tensor of 11 elements")
+    _check_out(x, out, bucket_offsets)
     with torch.cuda.device(x.device):
         _check(load().hs_merge(x.data_ptr(), out.data_ptr(), x.numel(), dt, bucket_offsets.data_ptr(),
                                chunks_per_bucket, _stream(stream)))

@@ -1,7 +1,12 @@
 // hs_api.cu -- the C ABI of libhybridsort.so (declared and documented in
 // include/hs.h): argument validation, stream-ordered scratch, and the launch
 // sequence of each entry point.  Every step of the method runs in the
-// kernels of hs_kernels.cu; this file only sequences them.
+// kernels of k_partition.cu, k_split.cu, k_tilesort.cu, k_merge.cu and
+// k_pairs.cu; this file only sequences them.
+//
+// HS_SPLIT (compile-time, default 1): the K5a value split of the chunks.
+// -DHS_SPLIT=0 builds the A/B variant without it (tools/exp.py); the product
+// library has no run-time switch.
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdint>
@@ -14,10 +19,15 @@
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
+#ifndef HS_SPLIT
+#define HS_SPLIT 1
+#endif
+
 namespace {
 
 thread_local char g_err[512] = "";
-thread_local int g_launches = 0;
+thread_local int g_launches = 0;         // kernels of the last successful call (hs_last_launch_count)
+thread_local int g_launch_counter = 0;   // kernels launched so far by the current call
 
 hs_status_t fail(hs_status_t s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 hs_status_t fail(hs_status_t s, const char *fmt, ...) {
@@ -32,7 +42,7 @@ hs_status_t cuda_fail(cudaError_t e, const char *what) {
     return fail(HS_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
-constexpr int kMaxDevices = 64;
+using hs::kMaxDevices;
 std::once_flag g_dev_once[kMaxDevices];
 int g_num_sms[kMaxDevices];
 
@@ -52,6 +62,11 @@ cudaError_t device_setup(int *num_sms) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
+        // kernel attributes and occupancy of the persistent kernels, once per device
+        if (err == cudaSuccess) err = hs::setup_partition_kernels(dev);
+        if (err == cudaSuccess) err = hs::setup_tilesort_kernels(dev);
+        if (err == cudaSuccess) err = hs::setup_merge_kernels(dev);
+        if (err == cudaSuccess) err = hs::setup_split_kernels(dev);
     });
     if (err != cudaSuccess) return err;
     *num_sms = g_num_sms[dev];
@@ -181,19 +196,23 @@ size_t samp_bytes(int64_t n, hs_dtype_t dt) { return (size_t)(n / hs::kSampleQ +
 #define HS_TRY_CUDA(expr, what)                                   \
     do {                                                          \
         cudaError_t _e = (expr);                                  \
-        ++launches;                                               \
         if (_e != cudaSuccess) {                                  \
             if (ws.base) cudaFreeAsync(ws.base, stream);          \
             return cuda_fail(_e, what);                           \
         }                                                         \
     } while (0)
 
-hs_status_t finish(Workspace &ws, cudaStream_t stream, int launches) {
-    cudaError_t e = cudaFreeAsync(ws.base, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
-    g_launches = launches;
+// A successful call: its kernel count becomes hs_last_launch_count().
+hs_status_t succeed() {
+    g_launches = g_launch_counter;
     g_err[0] = 0;
     return HS_OK;
+}
+
+hs_status_t finish(Workspace &ws, cudaStream_t stream) {
+    cudaError_t e = cudaFreeAsync(ws.base, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    return succeed();
 }
 
 // Merge levels the host must launch: each bucket runs L[b] <= this many
@@ -240,6 +259,8 @@ const char *const kProfNames[hs::kProfKinds] = {"tile_hist", "tile_scan", "scatt
 }  // namespace
 
 namespace hs {
+void note_launch() { ++g_launch_counter; }
+
 void prof_begin(int kind, cudaStream_t st) {
     (void)kind;
     if (!g_prof_on) return;
@@ -375,7 +396,7 @@ namespace {
 
 // a1-a3 on validated arguments.  key_shift: int64 items whose key is k >> 32.
 hs_status_t partition_impl(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift,
-                           int64_t *bucket_offsets, void *out, cudaStream_t stream, int *launches_out) {
+                           int64_t *bucket_offsets, void *out, cudaStream_t stream) {
     hs_status_t s;
     int sms;
     cudaError_t e = device_setup(&sms);
@@ -390,15 +411,12 @@ hs_status_t partition_impl(const void *keys, int64_t n, hs_dtype_t dtype, int nu
 
     Workspace ws;
     if ((s = ws_alloc(&ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, 0, stream)) != HS_OK) return s;
-    int launches = 0;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
     HS_TRY_CUDA(hs::launch_partition(dt, keys, out, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status,
                                      (long long *)bucket_offsets, -1, 0, 0, sms, true, stream, key_shift),
                 "K1-K3 partition");
-    launches += (tiles > 0 ? 2 : 0);  // K1, K2, K3 (K1/K3 skipped when n = 0)
     cudaError_t fe = cudaFreeAsync(ws.base, stream);
     if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
-    *launches_out = launches - 1;  // the memset is not one of our kernels
     return HS_OK;
 }
 
@@ -417,11 +435,9 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
     if (((uintptr_t)bucket_offsets & 7) != 0) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is not 8-byte aligned");
     if (n > 0 && overlap(keys, out, (size_t)n * ksize(dtype)))
         return fail(HS_ERR_INVALID_VALUE, "keys and out overlap (the partition is out of place)");
-    int launches = 0;
-    if ((s = partition_impl(keys, n, dtype, num_digits, 0, bucket_offsets, out, stream, &launches)) != HS_OK) return s;
-    g_launches = launches;
-    g_err[0] = 0;
-    return HS_OK;
+    g_launch_counter = 0;
+    if ((s = partition_impl(keys, n, dtype, num_digits, 0, bucket_offsets, out, stream)) != HS_OK) return s;
+    return succeed();
 }
 
 }  // extern "C"
@@ -433,7 +449,7 @@ namespace {
 // digit into those buckets -- a1-a3 are skipped, the plan comes from user_off,
 // the split reads keys and writes the scratch, the tile sort reads both.
 hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
-                      int log2c, cudaStream_t stream, int *launches_out, hs::Plan *inspect = nullptr,
+                      int log2c, cudaStream_t stream, hs::Plan *inspect = nullptr,
                       const int64_t *user_off = nullptr) {
     hs_status_t s;
     int sms;
@@ -448,11 +464,8 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     unsigned long long div, magic;
     digit_params(num_digits, key_shift ? HS_INT64 : dtype, &div, &magic);
 
-    // K5a value split of the chunks (on unless HS_SPLIT=0: A/B switch for measurements)
-    static const bool split_on = [] {
-        const char *e = getenv("HS_SPLIT");
-        return !(e && e[0] == '0');
-    }();
+    // K5a value split of the chunks (compile-time HS_SPLIT, see the top of this file)
+    constexpr bool split_on = HS_SPLIT != 0;
     const long long split_words = split_on ? hs::split_table_words(n, log2c, T) : 0;
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
@@ -464,10 +477,9 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         if (e2 == cudaSuccess)
             e2 = hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
                                       ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift);
-        int dummy = 0;
         if (e2 == cudaSuccess && split_on)
             e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
-                                  &dummy, stream);
+                                  stream);
         if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
         cudaError_t fe = cudaFreeAsync(ws.base, stream);
         if (e2 == cudaSuccess) e2 = fe;
@@ -475,7 +487,6 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         if (e2 != cudaSuccess) return cuda_fail(e2, "hs_sort_plan");
         return HS_OK;
     }
-    int launches = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
     // where the partitioned keys are (part) and where the split writes (spl)
@@ -483,7 +494,6 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     if (user_off) {
         // a4: plan from the caller's bucket offsets (keys already partitioned)
         HS_TRY_CUDA(hs::launch_plan((const long long *)user_off, ws.ctl, log2c, hs::kPlanSort, T, stream), "K4 plan");
-        ++launches;
         part = keys;
         spl = ws.S;
     } else {
@@ -491,12 +501,11 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         HS_TRY_CUDA(hs::launch_partition(dt, keys, ws.S, (int)n, h, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
                                          ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift),
                     "K1-K3 partition");
-        launches += 2;
     }
     // a5 (K5a): value split of every chunk that exceeds one tile, part -> spl
     if (split_on)
         HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, part, spl, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
-                                     key_shift, &launches, stream),
+                                     key_shift, stream),
                     "K5a split");
     // a5: leaf-tile sort (part, or spl for split buckets) -> (keys | S) per bucket parity
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
@@ -508,11 +517,9 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
                                            lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
-        ++launches;  // partition + merge
     }
     cudaError_t fe = cudaFreeAsync(ws.base, stream);
     if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
-    *launches_out = launches - 1;  // the memset is not one of our kernels
     return HS_OK;
 }
 
@@ -534,11 +541,9 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
         g_err[0] = 0;
         return HS_OK;
     }
-    int launches = 0;
-    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) return s;
-    g_launches = launches;
-    g_err[0] = 0;
-    return HS_OK;
+    g_launch_counter = 0;
+    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream)) != HS_OK) return s;
+    return succeed();
 }
 
 hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, const int64_t *bucket_offsets,
@@ -556,13 +561,11 @@ hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_dig
         g_err[0] = 0;
         return HS_OK;
     }
-    int launches = 0;
-    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &launches, nullptr,
-                       bucket_offsets)) != HS_OK)
+    g_launch_counter = 0;
+    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, nullptr, bucket_offsets)) !=
+        HS_OK)
         return s;
-    g_launches = launches;
-    g_err[0] = 0;
-    return HS_OK;
+    return succeed();
 }
 
 hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
@@ -577,9 +580,9 @@ hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_
     hs::Plan P;
     memset(&P, 0, sizeof(P));
     if (n > 0) {
-        int launches = 0;
-        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream,
-                           &launches, &P)) != HS_OK)
+        g_launch_counter = 0;
+        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &P)) !=
+            HS_OK)
             return s;
     }
     for (int b = 0; b < 10; ++b) {
@@ -615,6 +618,7 @@ hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dty
     int sms;
     cudaError_t e = device_setup(&sms);
     if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    g_launch_counter = 0;
     hs_partition_plan_s *p = new hs_partition_plan_s();
     p->keys = keys;
     p->n = n;
@@ -638,9 +642,7 @@ hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dty
         return cuda_fail(e, "K1-K2 count");
     }
     *plan = p;
-    g_launches = tiles > 0 ? 2 : 1;
-    g_err[0] = 0;
-    return HS_OK;
+    return succeed();
 }
 
 hs_status_t hs_partition_scatter(hs_partition_plan_t plan, void *const *dst, cudaStream_t stream) {
@@ -650,13 +652,12 @@ hs_status_t hs_partition_scatter(hs_partition_plan_t plan, void *const *dst, cud
         if (dst[d] && ((uintptr_t)dst[d] % ks) != 0)
             return fail(HS_ERR_INVALID_VALUE, "dst[%d] is not %d-byte aligned", d, ks);
     Workspace &ws = plan->ws;
+    g_launch_counter = 0;
     cudaError_t e = hs::launch_partition((int)plan->dtype, plan->keys, nullptr, (int)plan->n, plan->h, plan->div,
                                          plan->magic, ws.ctl, ws.tile_hist, ws.tile_pref, ws.status, nullptr, -1, 0, 0,
                                          plan->sms, true, stream, 0, false, dst);
     if (e != cudaSuccess) return cuda_fail(e, "K3 scatter");
-    g_launches = plan->n > 0 ? 1 : 0;
-    g_err[0] = 0;
-    return HS_OK;
+    return succeed();
 }
 
 hs_status_t hs_partition_plan_destroy(hs_partition_plan_t plan, cudaStream_t stream) {
@@ -691,12 +692,12 @@ hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, in
         return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed", 2 * ib + 256);
     }
     long long *items = (long long *)buf, *parted = (long long *)((char *)buf + round_up(ib, 256));
-    int launches = 0;
+    g_launch_counter = 0;
     if ((e = hs::launch_pack_items(keys, items, n, sms, stream)) != cudaSuccess) {
         cudaFreeAsync(buf, stream);
         return cuda_fail(e, "K0 pack items");
     }
-    if ((s = partition_impl(items, n, HS_INT64, num_digits, 32, bucket_offsets, parted, stream, &launches)) != HS_OK) {
+    if ((s = partition_impl(items, n, HS_INT64, num_digits, 32, bucket_offsets, parted, stream)) != HS_OK) {
         cudaFreeAsync(buf, stream);
         return s;
     }
@@ -706,9 +707,7 @@ hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, in
         return cuda_fail(e, "K8 unpack items");
     }
     if ((e = cudaFreeAsync(buf, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
-    g_launches = launches + (n > 0 ? 2 : 0);
-    g_err[0] = 0;
-    return HS_OK;
+    return succeed();
 }
 
 hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
@@ -737,13 +736,13 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
     }
     long long *items = (long long *)buf;
     unsigned long long *tag_copy = (unsigned long long *)((char *)buf + ib);
-    int launches = 0;
+    g_launch_counter = 0;
     if ((e = hs::launch_pack_items(keys, items, n, sms, stream)) != cudaSuccess ||
         (e = cudaMemcpyAsync(tag_copy, tags, (size_t)n * 8, cudaMemcpyDeviceToDevice, stream)) != cudaSuccess) {
         cudaFreeAsync(buf, stream);
         return cuda_fail(e, "K0 pack items / tag copy");
     }
-    if ((s = sort_impl(items, n, HS_INT64, num_digits, 32, chunks_per_bucket, log2c, stream, &launches)) != HS_OK) {
+    if ((s = sort_impl(items, n, HS_INT64, num_digits, 32, chunks_per_bucket, log2c, stream)) != HS_OK) {
         cudaFreeAsync(buf, stream);
         return s;
     }
@@ -753,9 +752,7 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
         return cuda_fail(e, "K8 unpack items");
     }
     if ((e = cudaFreeAsync(buf, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
-    g_launches = launches + 2;
-    g_err[0] = 0;
-    return HS_OK;
+    return succeed();
 }
 
 hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream) {
@@ -778,7 +775,7 @@ hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, 
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
         return s;
-    int launches = 0;
+    g_launch_counter = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan_whole(n, ws.ctl, log2c, T, stream), "K4 plan");
     // chunk sort: leaf tiles keys -> (keys | S) by parity, in place per leaf
@@ -789,9 +786,8 @@ hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, 
         HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
                                            lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
-        ++launches;
     }
-    return finish(ws, stream, launches);
+    return finish(ws, stream);
 }
 
 hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
@@ -819,7 +815,7 @@ hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtyp
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) != HS_OK)
         return s;
-    int launches = 0;
+    g_launch_counter = 0;
     const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(hs::launch_plan((const long long *)bucket_offsets, ws.ctl, log2c, hs::kPlanChunks, T, stream), "K4 plan");
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, in, out, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream),
@@ -829,9 +825,8 @@ hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtyp
         HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
                                            lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
-        ++launches;
     }
-    return finish(ws, stream, launches);
+    return finish(ws, stream);
 }
 
 hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
@@ -855,13 +850,11 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
     const int dt = (int)dtype;
     const int TM = hs::merge_span(dt);
     const long long nblocks = (n + TM - 1) / TM;
-    int launches = 0;
+    g_launch_counter = 0;
     Workspace ws;
     if (log2c == 0) {  // c = 1: zero rounds, out = in
         if (in != out) HS_TRY_CUDA(hs::launch_copy(dt, in, out, n, sms, stream), "K7 copy");
-        g_launches = launches;
-        g_err[0] = 0;
-        return HS_OK;
+        return succeed();
     }
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype), 0, 0, (size_t)nblocks + 2, samp_bytes(n, dtype), stream)) !=
         HS_OK)
@@ -880,9 +873,8 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
         HS_TRY_CUDA(hs::launch_merge_level(dt, plan, out, ws.S, src0, ws.corank, ws.samp[lv & 1],
                                            lv + 1 < log2c ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
-        ++launches;
     }
-    return finish(ws, stream, launches);
+    return finish(ws, stream);
 }
 
 }  // extern "C"

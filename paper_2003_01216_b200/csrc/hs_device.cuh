@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "hs_launch.h"
+
 // Device-side invariant checks of the debug build (libhybridsort_debug.so,
 // -DHS_DEBUG; tests/test_debug_build.py): shared-memory indices, piece
 // geometry, scatter positions.  compute-sanitizer is closed on this pool, so
@@ -92,7 +94,9 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e == cudaSuccess) note_launch();
+    return e;
 }
 
 // ------------------------------------------------------------------- plan

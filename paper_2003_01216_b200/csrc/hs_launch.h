@@ -17,6 +17,18 @@ enum ProfKind { kProfTileHist = 0, kProfTileScan, kProfScatter, kProfPlan, kProf
                 kProfMergeLevel, kProfCopy, kProfSplitCount, kProfSplitScatter, kProfKinds };
 void prof_begin(int kind, cudaStream_t st);
 void prof_end(int kind, cudaStream_t st);
+// Kernel launch accounting (hs_last_launch_count): every successful kernel
+// launch of the library calls note_launch() once, on the calling thread.
+void note_launch();
+
+// One-time per-device kernel configuration (dynamic shared-memory limits,
+// occupancy of the persistent kernels), run under hs_api.cu's per-device
+// std::call_once; the launchers only read what it stored.
+constexpr int kMaxDevices = 64;
+cudaError_t setup_partition_kernels(int dev);
+cudaError_t setup_tilesort_kernels(int dev);
+cudaError_t setup_merge_kernels(int dev);
+cudaError_t setup_split_kernels(int dev);
 
 int scatter_tile_keys(int dt);  // keys per K1/K3 tile
 int sort_tile_keys(int dt);     // leaf-tile capacity T of K5
@@ -40,10 +52,10 @@ cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F,
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +
 // plan finalisation, scatter pass S -> F.  tab / cur hold tab_words words
-// (zeroed by the caller before the count pass).  Returns the kernels launched.
+// (zeroed by k_split_setup before the count pass).
 long long split_table_words(long long n, int log2c, int tile_keys);
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
-                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, int *launches,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
                          cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
 // the samples this level writes for the next one (may be null).

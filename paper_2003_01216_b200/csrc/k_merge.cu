@@ -416,6 +416,26 @@ int merge_span_t() {
     return MGeo<K>::kNT * MGeo<K>::kVT;
 }
 
+int g_merge_per_sm[kMaxDevices][2];  // resident K6b CTAs per SM, per device: [int32, int64]
+
+template <typename K>
+cudaError_t setup_merge_t(int dev) {
+    using G = MGeo<K>;
+    using SM = MergeSmem<K, G::kNT, G::kVT, G::kST>;
+    auto kern = k_merge_level<K, G::kNT, G::kVT, G::kST>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::bytes());
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kNT + 32, SM::bytes());
+    g_merge_per_sm[dev][sizeof(K) == 8 ? 1 : 0] = occ > 0 ? occ : 1;
+    return e;
+}
+
+cudaError_t setup_merge_kernels(int dev) {
+    cudaError_t e = setup_merge_t<int32_t>(dev);
+    return e != cudaSuccess ? e : setup_merge_t<int64_t>(dev);
+}
+
 template <typename K>
 cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void *src0, int *corank,
                                  const void *samp_in, void *samp_out, int level, int n, int num_sms,
@@ -424,19 +444,10 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     using SM = MergeSmem<K, G::kNT, G::kVT, G::kST>;
     constexpr int TM = SM::TM;
     auto kern = k_merge_level<K, G::kNT, G::kVT, G::kST>;
-    static int configured_dev = -1;
-    static int per_sm = 1;
     int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_dev != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::bytes());
-        if (e != cudaSuccess) return e;
-        int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kNT + 32, SM::bytes());
-        if (e != cudaSuccess) return e;
-        per_sm = occ > 0 ? occ : 1;
-        configured_dev = dev;
-    }
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    const int per_sm = g_merge_per_sm[dev][sizeof(K) == 8 ? 1 : 0];
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
     const int nbounds = nblocks + 1;
@@ -458,6 +469,7 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
                                        (const K *)samp_in, corank, level, n, TM, nbounds);
     prof_end(kProfMergePartition, st);
     if (e != cudaSuccess) return e;
+    note_launch();
     long long grid = (long long)per_sm * num_sms;
     if (grid > nblocks) grid = nblocks;
     prof_begin(kProfMergeLevel, st);
@@ -468,6 +480,7 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
                            level, n, nblocks);
     prof_end(kProfMergeLevel, st);
     if (e != cudaSuccess) return e;
+    note_launch();
     return cudaGetLastError();
 }
 
@@ -478,7 +491,9 @@ cudaError_t launch_sample_t(const void *src, void *samp, long long n, cudaStream
     prof_begin(kProfMergePartition, st);
     k_sample<K><<<(unsigned)((m + 255) / 256), 256, 0, st>>>((const K *)src, (K *)samp, n);
     prof_end(kProfMergePartition, st);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) note_launch();
+    return e;
 }
 
 template <typename K>
@@ -489,7 +504,9 @@ cudaError_t launch_copy_t(const void *src, void *dst, long long n, int num_sms, 
     prof_begin(kProfCopy, st);
     k_copy<K><<<grid, 256, 0, st>>>((const K *)src, (K *)dst, n);
     prof_end(kProfCopy, st);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) note_launch();
+    return e;
 }
 
 int merge_span(int dt) { return dt == 0 ? merge_span_t<int32_t>() : merge_span_t<int64_t>(); }

@@ -44,7 +44,9 @@ cudaError_t launch_pack_items(const int32_t *keys, long long *items, long long n
     prof_begin(kProfCopy, st);
     k_pack_items<<<grid_for(n, num_sms), 256, 0, st>>>(keys, items, n);
     prof_end(kProfCopy, st);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) note_launch();
+    return e;
 }
 
 cudaError_t launch_unpack_items(const long long *items, int32_t *keys, const unsigned long long *tag_in,
@@ -53,7 +55,9 @@ cudaError_t launch_unpack_items(const long long *items, int32_t *keys, const uns
     prof_begin(kProfCopy, st);
     k_unpack_items<<<grid_for(n, num_sms), 256, 0, st>>>(items, keys, tag_in, tag_out, n);
     prof_end(kProfCopy, st);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) note_launch();
+    return e;
 }
 
 }  // namespace hs

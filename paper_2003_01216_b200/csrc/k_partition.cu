@@ -475,9 +475,37 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
                                                   s_dstart, s_delta, s_dptr, dtab);
         __syncthreads();  // stage / sOut / tables are reused next iteration
     }
+    // TABLE (hs_partition_scatter): the stores may target peer GPUs' memory;
+    // order them before whatever signals the peers next (dist.py: grid
+    // completion + a symmetric-memory barrier)
+    if (TABLE) __threadfence_system();
 }
 
 // =============================================================== launchers
+// resident K3 CTAs per SM, per device: [int32, int64] x [local CSR, destination table]
+int g_scatter_per_sm[kMaxDevices][4];
+
+template <typename K, bool TABLE>
+cudaError_t setup_scatter_t(int dev, int slot) {
+    using G = PGeo<K>;
+    using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
+    auto kern = k_scatter<K, G::kScatNT, G::kScatVT, TABLE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::bytes());
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kScatNT, SS::bytes());
+    g_scatter_per_sm[dev][slot] = occ > 0 ? occ : 1;
+    return e;
+}
+
+cudaError_t setup_partition_kernels(int dev) {
+    cudaError_t e;
+    if ((e = setup_scatter_t<int32_t, false>(dev, 0)) != cudaSuccess) return e;
+    if ((e = setup_scatter_t<int64_t, false>(dev, 1)) != cudaSuccess) return e;
+    if ((e = setup_scatter_t<int32_t, true>(dev, 2)) != cudaSuccess) return e;
+    return setup_scatter_t<int64_t, true>(dev, 3);
+}
+
 template <typename K>
 int scatter_tile_keys_t() {
     return PGeo<K>::kScatNT * PGeo<K>::kScatVT;
@@ -509,6 +537,7 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
         prof_end(kProfTileHist, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        note_launch();
     }
     const long long per = (long long)kScanNT * kScanIPT;
     const int sgrid = (int)(ntiles > 0 ? (ntiles + per - 1) / per : 1);
@@ -524,28 +553,17 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
     // local CSR output, or the destination-pointer table of hs_partition_scatter
     auto kern = dst10 ? k_scatter<K, G::kScatNT, G::kScatVT, true> : k_scatter<K, G::kScatNT, G::kScatVT, false>;
-    static int configured_dev[2] = {-1, -1};
-    static int per_sm[2] = {1, 1};
-    const int ki = dst10 ? 1 : 0;
     int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_dev[ki] != dev) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SS::bytes());
-        if (e != cudaSuccess) return e;
-        int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kScatNT, SS::bytes());
-        if (e != cudaSuccess) return e;
-        per_sm[ki] = occ > 0 ? occ : 1;
-        configured_dev[ki] = dev;
-    }
-    long long grid = (long long)per_sm[ki] * num_sms;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    const int ki = (dst10 ? 2 : 0) + (sizeof(K) == 8 ? 1 : 0);
+    long long grid = (long long)g_scatter_per_sm[dev][ki] * num_sms;
     if (grid > ntiles) grid = ntiles;
     prof_begin(kProfScatter, st);
     DstTable<K> dtab;
     dtab.use = dst10 != nullptr;
     for (int d = 0; d < 10; ++d) dtab.dst[d] = dst10 ? (K *)dst10[d] : nullptr;
-cudaError_t el = launch_pdl(kern, dim3((unsigned)grid), dim3(G::kScatNT), SS::bytes(), st, (const K *)keys, (K *)out, n, h, dp, ctl, tile_pref,
-                                                          (int)ntiles, dtab);
+    cudaError_t el = launch_pdl(kern, dim3((unsigned)grid), dim3(G::kScatNT), SS::bytes(), st, (const K *)keys,
+                                (K *)out, n, h, dp, ctl, tile_pref, (int)ntiles, dtab);
     if (el != cudaSuccess) return el;
     prof_end(kProfScatter, st);
     return cudaGetLastError();

@@ -710,10 +710,36 @@ static int nsb_bound(long long n, int log2c, int tile_keys) {
     return (int)(ns < kSplitMaxSub ? (ns < 2 ? 2 : ns) : kSplitMaxSub);
 }
 
+int g_split_sms[kMaxDevices];
+
+// dynamic shared memory of the count / scatter passes at the largest sub-range count (kSplitMaxSub)
+template <typename K>
+cudaError_t setup_split_t() {
+    using G = SplGeo<K>;
+    constexpr int TS = G::NT * G::VT;
+    const size_t sm_count = (size_t)(kSplitMaxSub + 1) * 4;
+    const size_t sm_scat = (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * 8 +
+                           (size_t)TS * (sizeof(K) + 4);
+    cudaError_t e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat);
+}
+
+cudaError_t setup_split_kernels(int dev) {
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    g_split_sms[dev] = sms > 0 ? sms : 148;
+    if ((e = setup_split_t<int32_t>()) != cudaSuccess) return e;
+    return setup_split_t<int64_t>();
+}
+
 template <typename K>
 static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uint32_t *cur, long long tab_words,
                                   long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
-                                  int *launches, cudaStream_t st) {
+                                  cudaStream_t st) {
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
     const int nsb_cap = nsb_bound(n, log2c, tile_keys);
@@ -723,13 +749,9 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT>;
     auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count)) != cudaSuccess)
-        return e;
-    if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat)) != cudaSuccess)
-        return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    const int sms = g_split_sms[dev];
     const long long c = 1LL << log2c;
     const long long grid = n / TS + 20 * c + 16;  // >= sum over buckets of c * ceil(chunk / TS)
     const long long tab_cap = tab_words - split_extra_words(log2c);
@@ -759,17 +781,16 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
         cudaSuccess)
         return e;
     prof_end(kProfSplitScatter, st);
-    *launches += 5;
     return cudaGetLastError();
 }
 
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
-                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, int *launches,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
                          cudaStream_t st) {
     return dt == 0 ? launch_split_t<int32_t>(ctl, (const int32_t *)S, (int32_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, launches, st)
+                                             tile_keys, div, key_shift, st)
                    : launch_split_t<int64_t>(ctl, (const int64_t *)S, (int64_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, launches, st);
+                                             tile_keys, div, key_shift, st);
 }
 
 }  // namespace hs

@@ -528,6 +528,20 @@ struct SGeo<int64_t> {
     static constexpr int kBuckets = HS_SORT_BUCKETS64 * HS_SORT_NT64, kCap = HS_SORT_CAP64;
 };
 
+template <typename K>
+cudaError_t setup_tile_sort_t() {
+    using G = SGeo<K>;
+    constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
+    return cudaFuncSetAttribute(k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t setup_tilesort_kernels(int dev) {
+    (void)dev;
+    cudaError_t e = setup_tile_sort_t<int32_t>();
+    return e != cudaSuccess ? e : setup_tile_sort_t<int64_t>();
+}
+
 int sort_tile_keys(int dt) {
     return dt == 0 ? SGeo<int32_t>::kNT * SGeo<int32_t>::kVT : SGeo<int64_t>::kNT * SGeo<int64_t>::kVT;
 }
@@ -554,14 +568,6 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
-    static int configured_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_dev != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured_dev = dev;
-    }
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)max_tiles), dim3(G::kNT), smem, st, plan, (const K *)src, (K *)F,

@@ -155,21 +155,24 @@ def exchange_layout(sizes, group_start):
 
 
 class _SymmBuffer:
-    """Cached symmetric-memory receive buffer (re-made only when it must grow)."""
+    """Cached symmetric-memory receive buffers, one per (dtype, device, process
+    group); a buffer is re-made only when it must grow.  The buffer is the
+    library's: dist_sort_fused hands the caller a copy, never a view of it."""
 
     def __init__(self):
-        self.buf = self.handle = None
-        self.key = None
+        self.entries = {}
 
     def get(self, numel, dtype, device, group):
+        import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
-        if self.buf is None or self.buf.numel() < numel or self.key != (dtype, device):
-            cap = max(numel, 1)
-            import torch.distributed as dist
-            self.buf = symm_mem.empty(cap, dtype=dtype, device=device)
-            self.handle = symm_mem.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
-            self.key = (dtype, device)
-        return self.buf, self.handle
+        pg = group if group is not None else dist.group.WORLD
+        key = (dtype, str(device), id(pg))
+        ent = self.entries.get(key)
+        if ent is None or ent[0].numel() < numel:
+            buf = symm_mem.empty(max(numel, 1), dtype=dtype, device=device)
+            ent = (buf, symm_mem.rendezvous(buf, pg), pg)  # pg kept alive with its handle
+            self.entries[key] = ent
+        return ent[0], ent[1]
 
 
 _SYMM = _SymmBuffer()
@@ -182,7 +185,18 @@ def dist_sort_fused(keys, num_digits: int, chunks: int = 8, group=None):
     symmetric-memory receive buffer over NVLink (peer stores from the kernel,
     hs_partition_scatter) -- no all-to-all call and no staging copy; then every
     owner chunk-sorts and tree-merges its received buckets in place.  Returns
-    (local_sorted view, DistInfo).  CUDA + NCCL process group only.
+    (local_sorted, DistInfo); local_sorted is a tensor the caller owns (a copy
+    out of the cached receive buffer, which the next call overwrites).  CUDA +
+    NCCL process group only.
+
+    Cross-GPU ordering: (1) handle.barrier() before the scatter
+    -- no rank's K3 stores into an owner's buffer until every rank has finished
+    with the previous call's contents; (2) K3 ends with a system-scope fence
+    (__threadfence_system) after its last peer store, and the host waits for
+    the K3 grid to complete (stream synchronize); (3) handle.barrier() after it
+    -- a release/acquire signal exchange among all ranks, so when an owner
+    passes it every rank's stores into its buffer have completed and are
+    visible; only then does the owner's hs_sort_buckets read the buffer.
     """
     import torch
     import torch.distributed as dist
@@ -218,6 +232,7 @@ def dist_sort_fused(keys, num_digits: int, chunks: int = 8, group=None):
     if n_local:
         roff = torch.tensor(recv_offsets[rank], dtype=torch.int64, device=keys.device)
         hs_sort_buckets(local, roff, num_digits, chunks)  # chunk sort (+ value split) + tree merge, in place
+    local = local.clone()  # owned by the caller: the receive buffer is reused by the next call
     send = [sum(sizes[rank][d] for d in range(10) if owner[d] == g) for g in range(world)]
     recv = [sum(sizes[r][d] for d in range(10) if owner[d] == rank) for r in range(world)]
     return local, DistInfo(group_start, global_sizes, send, recv, max_load)

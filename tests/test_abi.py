@@ -116,3 +116,41 @@ def test_python_binding_refuses_cpu_tensors():
 def test_missing_library_fails_loudly(tmp_path):
     with pytest.raises(RuntimeError):
         hs.load(str(tmp_path / "nope.so"))
+
+
+class _FakeTensor:
+    """Just the attributes the binding's argument checks read (no device needed)."""
+
+    def __init__(self, dtype, numel, device="cuda:0"):
+        import torch
+        self.dtype, self._n, self.device, self.is_cuda = dtype, numel, torch.device(device), True
+
+    def numel(self):
+        return self._n
+
+    def is_contiguous(self):
+        return True
+
+
+def test_binding_rejects_short_or_mismatched_out():
+    """hs_sort_chunks / hs_merge write n * itemsize bytes into out (the C ABI takes n from x):
+    the binding must refuse an out that is shorter, of another dtype or on another device."""
+    import torch
+    x = _FakeTensor(torch.int32, 1000)
+    off = _FakeTensor(torch.int64, 11)
+    hs._check_out(x, _FakeTensor(torch.int32, 1000), off)  # matching: accepted
+    for bad in (_FakeTensor(torch.int32, 999), _FakeTensor(torch.int64, 1000), _FakeTensor(torch.int32, 1000, "cuda:1")):
+        with pytest.raises(ValueError, match="out must match"):
+            hs._check_out(x, bad, off)
+    with pytest.raises(ValueError, match="bucket_offsets"):
+        hs._check_out(x, _FakeTensor(torch.int32, 1000), _FakeTensor(torch.int64, 11, "cuda:1"))
+    with pytest.raises(ValueError, match="bucket_offsets"):
+        hs._check_out(x, _FakeTensor(torch.int32, 1000), _FakeTensor(torch.int32, 11))
+
+
+def test_library_has_no_runtime_switches():
+    """The C ABI's behaviour depends on its arguments only: no environment variable picks a path."""
+    csrc = os.path.join(ROOT, "paper_2003_01216_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in src, f  # (the statically linked cudart reads CUDA_* variables itself)
