@@ -117,8 +117,8 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 //    value into nsb[b] sub-ranges, each at most T keys; the tile-sort leaves
 //    are those sub-ranges (bounds in the split table at sboff[b]), k[b] = 0
 //    and the merge levels are only the paper's chunk tree (L[b] = log2 c).
-//  * tree[b] = 1 (a split bucket with equal-width sub-ranges and an odd
-//    log2 c <= 5, k_tree.cu): sub-range t covers the same key interval in
+//  * tree[b] = 1 (a split bucket with equal-width sub-ranges and c = 2 or 8,
+//    k_tree.cu): sub-range t covers the same key interval in
 //    every chunk, so the chunk tree of the bucket is run per (sub-range, key
 //    segment) on chip -- all log2 c rounds in one HBM pass -- unless the tree
 //    plan finds a segment over capacity (ctl->treebad), in which case the
@@ -140,7 +140,7 @@ struct Plan {
 // equal-width sub-range is cut into kTreeFine equal fine bins; the tile sort
 // of every piece records e[u] = #keys of the piece in bins <= u.
 constexpr int kTreeFineLog2 = 10, kTreeFine = 1 << kTreeFineLog2;
-constexpr int kTreeMaxLog2C = 5;
+constexpr int kTreeMaxLog2C = 3;  // c <= 8: the tree merge's shared-memory layout
 
 // K5a bookkeeping (value split of the chunks), written by k_split_setup and
 // k_split_map.  Fine bins: kSplitFine equal-width bins of a bucket's digit

@@ -86,13 +86,25 @@ __device__ __forceinline__ bool level_active(const Plan &P, int b, int level, un
     return level < P.L[b] && !(P.tree[b] && !((tbad >> b) & 1u));
 }
 
+// Does any bucket run this level?  (Read straight from the global plan, so a
+// launch past the device plan -- the host only knows a bound -- exits at once.)
+__device__ __forceinline__ bool level_any(const Plan *__restrict__ g, int level, const unsigned *treebad) {
+    if (level >= __ldg(&g->Lmax)) return false;
+    const unsigned tbad = treebad ? *treebad : ~0u;
+    bool any = false;
+#pragma unroll
+    for (int b = 0; b < 10; ++b)
+        any |= level < __ldg(&g->L[b]) && !(__ldg(&g->tree[b]) && !((tbad >> b) & 1u));
+    return any;
+}
+
 template <typename K>
 __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
                                   const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds,
                                   const unsigned *treebad) {
     constexpr long long Q = kSampleQ;
     griddep_wait();
-    if (level >= __ldg(&plan_g->Lmax)) return;  // no bucket runs this level (the host only knows a bound)
+    if (!level_any(plan_g, level, treebad)) return;  // no bucket runs this level (the host only knows a bound)
     __shared__ Plan P;
     load_plan_m(P, plan_g);
     const unsigned tbad = treebad ? *treebad : ~0u;
@@ -222,7 +234,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     const K kMax = KeyTraits<K>::kMax;
 
     griddep_wait();
-    if (level >= __ldg(&plan_g->Lmax)) return;  // whole CTA: nothing at this level
+    if (!level_any(plan_g, level, treebad)) return;  // whole CTA: nothing at this level
     load_plan_m(P, plan_g);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {

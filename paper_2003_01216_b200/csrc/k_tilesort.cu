@@ -169,16 +169,22 @@ __device__ __forceinline__ int tree_bin(int64_t k, int shift, long long lo, unsi
     return (int)((d * mul) >> (64 - kTreeFineLog2));
 }
 
-// e[u] = #keys of the sorted piece so[0, len) with tree bin <= u, u < kTreeFine:
-// position p (0 <= p <= len) is e[u] for u in [bin(p-1), bin(p)) (bin(-1) = -1,
-// bin(len) = kTreeFine), so every u is written exactly once.
+// e[u] = #keys of the sorted piece so[0, len) with tree bin <= u, u < kTreeFine,
+// by binary search (pieces whose bucket pass did not run on the tree bins:
+// edge sub-ranges, narrow ones, tiles that took the merge rounds).  A piece
+// whose bucket pass ran on the fraction bins writes e from its bucket counts
+// instead (they are the same bins).
 template <typename K>
 __device__ __forceinline__ void write_tree_prefix(uint16_t *e, const K *so, int len, long long lo,
                                                   unsigned long long mul, int shift, int t, int tid, int nthreads) {
-    for (int p = tid; p <= len; p += nthreads) {
-        const int up = p < len ? tree_bin(so[p], shift, lo, mul, t) : kTreeFine;
-        const int ub = p > 0 ? tree_bin(so[p - 1], shift, lo, mul, t) : 0;
-        for (int u = ub; u < up; ++u) e[u] = (uint16_t)p;
+    for (int u = tid; u < kTreeFine; u += nthreads) {
+        int l = 0, r = len;  // first position whose bin exceeds u
+        while (l < r) {
+            const int mid = (l + r) >> 1;
+            if (tree_bin(so[mid], shift, lo, mul, t) <= u) l = mid + 1;
+            else r = mid;
+        }
+        e[u] = (uint16_t)l;
     }
 }
 
@@ -551,8 +557,16 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         for (int p = tid; p < len; p += NT) out[p] = so[p];
     }
     write_samples(samp, lo, len, so, tid, NT);  // coarse index for merge level 0's co-rank search
-    if (tree_t >= 0)
-        write_tree_prefix(etab + g * kTreeFine, so, len, scfg->lo[b], scfg->mul[b], scfg->shift, tree_t, tid, NT);
+    if (tree_t >= 0) {
+        uint16_t *const e = etab + g * kTreeFine;
+        if (frac && mode == 2 && BUCKETS == kTreeFine && BPT_ == 2) {
+            // the bucket pass ran on the fraction bins = the tree bins: e from my two buckets' ends
+            const uint32_t e0 = bk_base + bk_cnt[0], e1 = e0 + bk_cnt[BPT_ - 1];
+            reinterpret_cast<uint32_t *>(e)[tid] = e0 | (e1 << 16);
+        } else {
+            write_tree_prefix(e, so, len, scfg->lo[b], scfg->mul[b], scfg->shift, tree_t, tid, NT);
+        }
+    }
 }
 
 // =============================================================== launchers

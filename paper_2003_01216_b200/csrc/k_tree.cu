@@ -39,14 +39,14 @@ template <typename K>
 struct TreeGeo;
 template <>
 struct TreeGeo<int32_t> {
-    static constexpr int NC = 256, VT = 17;  // CAP = 4352 keys per segment
+    static constexpr int NC = 256, VT = 17;  // CAP = 4352 keys per segment (VT odd: see V below)
 };
 template <>
 struct TreeGeo<int64_t> {
     static constexpr int NC = 256, VT = 9;   // CAP = 2304 keys per segment
 };
 constexpr int kTreeMaxC = 1 << kTreeMaxLog2C;
-constexpr int kTreeST = 2;  // stage slots
+constexpr int kTreeST = 3;  // stage slots
 
 template <typename K>
 struct TreeSmem {
@@ -54,10 +54,14 @@ struct TreeSmem {
     static constexpr int CAP = NC * VT;
     static constexpr int TGT = CAP * 3 / 4;  // segment target: room for one fine bin of CAP / 4 keys
     static constexpr int E = 16 / sizeof(K);
+    // every run in shared memory is followed by GAP kMax sentinels, so a thread's VT merge steps
+    // never need a bounds test (an exhausted run keeps reading kMax)
+    static constexpr int GAP = (VT + E - 1) / E * E;
     // a slot holds the c slices' 16-byte aligned supersets (each <= len + 2E - 2 keys, rounded to E)
-    static constexpr int SLOT = CAP + 2 * E * kTreeMaxC;
-    static constexpr int BUF = CAP + E;  // + the destination's 16-byte phase
-    static constexpr size_t bytes() { return (size_t)(kTreeST * SLOT + 2 * BUF) * sizeof(K); }
+    // + their gaps, later the even rounds' output; Y the odd rounds' (+ the destination's 16-byte phase)
+    static constexpr int SLOT = CAP + (2 * E + GAP) * kTreeMaxC;
+    static constexpr int BUF = CAP + GAP * kTreeMaxC / 2 + 2 * E;
+    static constexpr size_t bytes() { return (size_t)(kTreeST * SLOT + BUF) * sizeof(K); }
 };
 
 struct TreeSeg {
@@ -178,7 +182,6 @@ template <typename K>
 struct TreePiece {
     long long out;  // first output position (absolute)
     int M;          // keys in the segment (< 0: no more segments)
-    int c;
     int off[kTreeMaxC];  // slice j starts at stage + off[j]
     int len[kTreeMaxC];
 };
@@ -188,41 +191,145 @@ __device__ __forceinline__ void tree_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Merge-path split of output diag between A[0..na) and B[0..nb) (stable-left: ties take A).
 template <typename K>
-__device__ __forceinline__ int tree_path(const K *A, int na, const K *B, int nb, int diag) {
+__device__ __forceinline__ K tlds(uint32_t a);
+template <>
+__device__ __forceinline__ int32_t tlds<int32_t>(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+template <>
+__device__ __forceinline__ int64_t tlds<int64_t>(uint32_t a) {
+    int64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+template <typename K>
+__device__ __forceinline__ void tsts(uint32_t a, K v);
+template <>
+__device__ __forceinline__ void tsts<int32_t>(uint32_t a, int32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+template <>
+__device__ __forceinline__ void tsts<int64_t>(uint32_t a, int64_t v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+// Merge-path split of output diag between A[0..na) and B[0..nb) at shared
+// addresses ua / ub (stable-left: ties take A).
+template <typename K>
+__device__ __forceinline__ int tree_path(uint32_t ua, int na, uint32_t ub, int nb, int diag) {
+    constexpr int W = sizeof(K);
     int l = diag - nb > 0 ? diag - nb : 0;
     int r = diag < na ? diag : na;
     while (l < r) {
         const int mid = (l + r) >> 1;
-        if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
-        else r = mid;
+        const bool pr = tlds<K>(ua + mid * W) <= tlds<K>(ub + (diag - 1 - mid) * W);
+        l = pr ? mid + 1 : l;
+        r = pr ? r : mid;
     }
     return l;
 }
 
+// Outputs [p, pe) of one round.  Pair q (runs at shared addresses rA[q] /
+// rB[q], lengths rl[2q], rl[2q+1], each followed by >= VT kMax sentinels)
+// is merged from the merge-path split of p (stable-left); its output run
+// starts at shared address uo + (Oq + q gap) s.  Every thread runs VT merge
+// steps and stores the first cnt: no bounds tests (an exhausted run reads
+// kMax -- an exhausted A then only wins ties against a real kMax in B, with
+// the same value -- and at most VT steps past a run end stay in its gap).
+template <typename K, int VT>
+__device__ __forceinline__ void tree_round_outputs(int p, int pe, const int *rl, int npairs, const uint32_t *rA,
+                                                   const uint32_t *rB, uint32_t uo, int gap) {
+    constexpr int W = sizeof(K);
+    if (p >= pe) return;
+    int q = 0, Oq = 0;
+    int na = rl[0], nb = rl[1];
+    while (Oq + na + nb <= p && q + 1 < npairs) {
+        Oq += na + nb;
+        ++q;
+        na = rl[2 * q];
+        nb = rl[2 * q + 1];
+    }
+    for (;;) {
+        const uint32_t ua = rA[q], ub = rB[q];
+        const int diag = p - Oq;
+        const int a0 = tree_path<K>(ua, na, ub, nb, diag);
+        uint32_t pa = ua + a0 * W, pb = ub + (diag - a0) * W;
+        K x = tlds<K>(pa), y = tlds<K>(pb);
+        const int kend = min(pe, Oq + na + nb), cnt = kend - p;
+        const uint32_t o = uo + (p + q * gap) * W;
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {
+            const bool tA = x <= y;
+            if (k < cnt) tsts<K>(o + k * W, tA ? x : y);
+            if (k + 1 < VT) {
+                pa += tA ? W : 0;
+                pb += tA ? 0 : W;
+                const K t = tlds<K>(tA ? pa : pb);
+                x = tA ? t : x;
+                y = tA ? y : t;
+            }
+        }
+        p = kend;
+        if (p >= pe) return;
+        Oq += na + nb;  // my outputs continue in the next pair
+        ++q;
+        na = rl[2 * q];
+        nb = rl[2 * q + 1];
+    }
+}
+
+// Mbarrier phase wait with a suspend-time hint: a waiting thread sleeps in
+// hardware until the phase completes instead of re-issuing the try_wait.
+__device__ __forceinline__ void tree_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra TW_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
+// Persistent, warp-specialised; CTA blk owns the contiguous segment range
+// [blk * per, (blk + 1) * per) (consecutive segments of a sub-range share
+// their tables' cache lines).
+//   producer warp: geometry of the next segment (lane j <-> chunk j: split
+//     table, fine-bin prefixes) is loaded BEFORE waiting for a free stage
+//     slot, then the c slices are fetched by 1-D bulk async copies (16-byte
+//     aligned supersets) into the slot (ST slots, full/empty mbarriers);
+//   consumer warps: log2 c rounds -- round r merges run pairs (2q, 2q+1) into
+//     run q; odd rounds write Y, even rounds write the stage slot itself
+//     (its slices are consumed by round 0), so the last round (odd count)
+//     lands in Y at the destination's 16-byte phase; the slot is released
+//     after the last round, Y leaves with one bulk async store.
 template <typename K>
-__global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *__restrict__ ctl,
+__global__ void __launch_bounds__(TreeGeo<K>::NC + 32, 2) k_tree_merge(const Ctl *__restrict__ ctl,
                                                                   const uint32_t *__restrict__ sbtab,
                                                                   const uint16_t *__restrict__ etab,
                                                                   const TreeSeg *__restrict__ seg, long long seg_cap,
                                                                   const K *S, K *F) {
     using G = TreeSmem<K>;
-    constexpr int NC = G::NC, VT = G::VT, E = G::E, SLOT = G::SLOT, BUF = G::BUF;
+    constexpr int NC = G::NC, VT = G::VT, E = G::E, SLOT = G::SLOT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     K *const stage0 = reinterpret_cast<K *>(smem_raw);
-    K *const X = stage0 + kTreeST * SLOT;
-    K *const Y = X + BUF;
+    K *const Y = stage0 + kTreeST * SLOT;
     __shared__ __align__(8) uint64_t full[kTreeST];
     __shared__ __align__(8) uint64_t empty[kTreeST];
     __shared__ Plan P;
     __shared__ TreePiece<K> pc[kTreeST];
-    __shared__ int rl[kTreeMaxC];  // run lengths of the current round
+    __shared__ int rlb[2][kTreeMaxC];       // run lengths of the current / next round
+    __shared__ uint32_t rA[kTreeMaxC / 2];  // run pair q of the current round: shared addresses of A and B
+    __shared__ uint32_t rB[kTreeMaxC / 2];
     const int tid = threadIdx.x;
 
     griddep_wait();  // PDL: the tree plan (and the tile sort before it) is complete
-    const unsigned nseg = (unsigned)min((long long)ctl->nseg, seg_cap);
-    if (blockIdx.x >= nseg) return;
+    const long long nseg = min((long long)ctl->nseg, seg_cap);
+    const long long per = (nseg + gridDim.x - 1) / gridDim.x;
+    const long long i0 = (long long)blockIdx.x * per, i1 = min(i0 + per, nseg);
+    if (i0 >= i1) return;
     {
         constexpr int W = sizeof(Plan) / 4;
         const uint32_t *src = reinterpret_cast<const uint32_t *>(&ctl->plan);
@@ -238,41 +345,30 @@ __global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *_
     }
     __syncthreads();
     const unsigned tbad = ctl->treebad;
+    const int c = 1 << P.log2c;
 
     if (tid >= NC) {
         // ------------------------------------------------------------ producer warp
         const int lane = tid & 31;
-        const int c = 1 << P.log2c;
         int it = 0;
-        for (unsigned i = blockIdx.x;; i += gridDim.x) {
+        for (long long i = i0;; ++i) {
             int b = 0, t = 0;
             TreeSeg q;
             bool have = false;
-            while (i < nseg) {  // next segment of a bucket that takes the on-chip tree
+            for (; i < i1; ++i) {  // next segment of a bucket that takes the on-chip tree
                 q = seg[i];
                 tree_subrange(P, q.s, b, t);
                 if (!((tbad >> b) & 1u)) {
                     have = true;
                     break;
                 }
-                i += gridDim.x;
             }
-            const int slot = it % kTreeST;
-            mbar_wait(&empty[slot], ((it / kTreeST) & 1) ^ 1);
-            if (!have) {
-                if (lane == 0) {
-                    pc[slot].M = -1;
-                    mbar_arrive_expect_tx(&full[slot], 0);
-                }
-                return;
-            }
-            const int ns = P.nsb[b];
-            const int u0 = q.u01 & 0xFFFF, u1 = q.u01 >> 16;
-            const long long m = P.off[b + 1] - P.off[b];
-            // lane j: chunk j's slice of the segment
             int len = 0, outpart = 0;
             const K *src = S;
-            if (lane < c) {
+            if (have && lane < c) {  // lane j: chunk j's slice of the segment
+                const int ns = P.nsb[b];
+                const int u0 = q.u01 & 0xFFFF, u1 = q.u01 >> 16;
+                const long long m = P.off[b + 1] - P.off[b];
                 const uint32_t st = __ldg(sbtab + P.sboff[b] + (long long)lane * (ns + 1) + t);
                 const uint16_t *e = etab + (size_t)(P.tile_prefix[b] + (long long)lane * ns + t) * kTreeFine;
                 const int e0 = u0 ? (int)__ldg(e + u0 - 1) : 0;
@@ -281,23 +377,32 @@ __global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *_
                 outpart = (int)st + e0;
                 src = S + P.off[b] + part_start(m, P.log2c, lane) + st + e0;
             }
+            const int slot = it % kTreeST;
+            tree_wait(&empty[slot], ((it / kTreeST) & 1) ^ 1);
+            if (!have) {
+                if (lane == 0) {
+                    pc[slot].M = -1;
+                    mbar_arrive_expect_tx(&full[slot], 0);
+                }
+                return;
+            }
             const uintptr_t ga0 = (uintptr_t)src & ~(uintptr_t)15;
             const uintptr_t ga1 = ((uintptr_t)(src + len) + 15) & ~(uintptr_t)15;
             const int words = len > 0 ? (int)((ga1 - ga0) / sizeof(K)) : 0;  // multiple of E
-            int incl = words;
+            int incl = lane < c ? words + G::GAP : 0;  // each slice region + its sentinel gap
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            const int region = incl - words;
+            const int region = incl - (lane < c ? words + G::GAP : 0);
             int M = len, outsum = outpart;
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) {
                 M += __shfl_xor_sync(0xffffffffu, M, o);
                 outsum += __shfl_xor_sync(0xffffffffu, outsum, o);
             }
-            const int total_words = __shfl_sync(0xffffffffu, incl, 31);
+            const int total_words = __shfl_sync(0xffffffffu, incl, 31);  // (incl. gaps: not transferred)
             TreePiece<K> &d = pc[slot];
             if (lane < c) {
                 d.off[lane] = region + (int)(((uintptr_t)src - ga0) / sizeof(K));
@@ -305,12 +410,14 @@ __global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *_
             }
             if (lane == 0) {
                 d.M = M;
-                d.c = c;
                 d.out = P.off[b] + outsum;
             }
+            int tx = words;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
             HS_DASSERT(M <= G::CAP && total_words <= SLOT);
             __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)total_words * sizeof(K));
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)tx * sizeof(K));
             __syncwarp();
             if (words > 0) bulk_g2s(stage0 + slot * SLOT + region, (const void *)ga0, (uint32_t)words * sizeof(K),
                                     &full[slot]);
@@ -320,93 +427,63 @@ __global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *_
 
     // ---------------------------------------------------------------- consumers
     const K kMax = KeyTraits<K>::kMax;
+    constexpr int GAP = G::GAP;
     for (int it = 0;; ++it) {
         const int slot = it % kTreeST;
-        mbar_wait(&full[slot], (it / kTreeST) & 1);
+        tree_wait(&full[slot], (it / kTreeST) & 1);
         const TreePiece<K> &d = pc[slot];
         const int M = d.M;
         if (M < 0) break;
-        const int c = d.c;
-        const K *sb = stage0 + slot * SLOT;
+        K *const sb = stage0 + slot * SLOT;
         K *const out = F + d.out;
         const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // last store done reading
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Y free again
+        int *rl = rlb[0];
         if (tid < c) rl[tid] = d.len[tid];
+        const uint32_t usb = smem_u32(sb), uY = smem_u32(Y);
+        if (tid < c / 2) {
+            rA[tid] = usb + d.off[2 * tid] * (uint32_t)sizeof(K);
+            rB[tid] = usb + d.off[2 * tid + 1] * (uint32_t)sizeof(K);
+        }
+        for (int k = tid; k < c * GAP; k += NC) sb[d.off[k / GAP] + d.len[k / GAP] + k % GAP] = kMax;  // sentinels
         tree_bar(NC);
-        // rounds: runs (2q, 2q+1) -> run q; round 1 reads the stage slices, later rounds the
-        // previous round's buffer (runs contiguous); the last round writes at the phase sh
+        // outputs per thread this segment: balanced rounds; odd, so a warp's output runs (stride V) hit
+        // 32 distinct banks (V <= VT since M <= NC VT and VT is odd)
+        const int V = ((M + NC - 1) / NC) | 1;
         int nruns = c;
-        const K *in = nullptr;
-        K *dst = Y;
         for (int r = 0; (1 << r) < c; ++r) {
             const bool last = (2 << r) >= c;
-            K *const o = dst + (last ? sh : 0);
-            // my outputs [p, pe)
-            int p = tid * VT;
-            const int pe = min(p + VT, M);
-            // find the pair holding p: prefix over pairs
-            int q = 0, Oq = 0;
-            int na = 0, nb = 0;
-            auto load_pair = [&](int qq) {
-                na = rl[2 * qq];
-                nb = rl[2 * qq + 1];
-            };
-            int runoff = 0;  // start of run 2q in the previous round's buffer
-            if (p < pe) {
-                load_pair(0);
-                while (Oq + na + nb <= p) {
-                    Oq += na + nb;
-                    ++q;
-                    load_pair(q);
+            K *const ob = (r & 1) ? sb : Y + (last ? sh : 0);
+            const uint32_t uo = smem_u32(ob);
+            tree_round_outputs<K, VT>(tid * V, min(tid * V + V, M), rl, nruns / 2, rA, rB, uo, GAP);
+            tree_bar(NC);  // round complete
+            if (!last) {
+                // the next round's runs: merged pair q at (its output prefix + q GAP), GAP sentinels after it
+                for (int k = tid; k < (nruns / 2) * GAP; k += NC) {
+                    const int q = k / GAP;
+                    int pre = 0;
+                    for (int j = 0; j <= 2 * q + 1; ++j) pre += rl[j];
+                    ob[pre + q * GAP + k % GAP] = kMax;
                 }
-                runoff = Oq;
-            }
-            while (p < pe) {
-                const K *A, *B;
-                if (r == 0) {
-                    A = sb + d.off[2 * q];
-                    B = sb + d.off[2 * q + 1];
-                } else {
-                    A = in + runoff;
-                    B = in + runoff + na;
-                }
-                const int diag = p - Oq;
-                const int a0 = tree_path(A, na, B, nb, diag);
-                int ai = a0, bi = diag - a0;
-                const int kend = min(pe, Oq + na + nb);
-                K x = ai < na ? A[ai] : kMax;
-                K y = bi < nb ? B[bi] : kMax;
-                for (; p < kend; ++p) {
-                    const bool tA = bi >= nb || (ai < na && x <= y);
-                    o[p] = tA ? x : y;
-                    if (tA) {
-                        ++ai;
-                        x = ai < na ? A[ai] : kMax;
-                    } else {
-                        ++bi;
-                        y = bi < nb ? B[bi] : kMax;
+                int *const rn = rlb[(r + 1) & 1];  // (rl is still read by the sentinel writers)
+                if (tid == 0) {
+                    int pre = 0;
+                    for (int k = 0; k < nruns / 4; ++k) {
+                        const int la = rl[4 * k] + rl[4 * k + 1], lb = rl[4 * k + 2] + rl[4 * k + 3];
+                        rA[k] = uo + (pre + 2 * k * GAP) * (uint32_t)sizeof(K);
+                        rB[k] = uo + (pre + la + (2 * k + 1) * GAP) * (uint32_t)sizeof(K);
+                        pre += la + lb;
+                        rn[2 * k] = la;
+                        rn[2 * k + 1] = lb;
                     }
                 }
-                if (p < pe) {  // next pair
-                    Oq += na + nb;
-                    runoff = Oq;
-                    ++q;
-                    load_pair(q);
-                }
-            }
-            tree_bar(NC);  // round complete: every thread read its inputs
-            if (r == 0 && (tid & 31) == 0) tree_arrive(&empty[slot]);  // stage slot free for the next segment
-            // next round's runs
-            if (tid == 0) {
-                for (int k = 0; k < nruns / 2; ++k) rl[k] = rl[2 * k] + rl[2 * k + 1];
+                rl = rn;
             }
             nruns >>= 1;
-            in = dst;
-            dst = (dst == Y) ? X : Y;
             tree_bar(NC);
         }
-        // the sorted segment sits at in[sh .. sh + M): bulk store the aligned middle
-        const K *so = in;
+        if ((tid & 31) == 0) tree_arrive(&empty[slot]);  // the slot (inputs and even rounds) is free
+        // the sorted segment sits at Y[sh .. sh + M): bulk store the aligned middle
         fence_proxy_async_smem();
         tree_bar(NC);
         const int end = sh + M;
@@ -416,19 +493,19 @@ __global__ void __launch_bounds__(TreeGeo<K>::NC + 32) k_tree_merge(const Ctl *_
         if (m1 > m0) {
             if (tid == 0) {
                 asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g + m0),
-                             "r"(smem_u32(so + m0)), "r"((uint32_t)((m1 - m0) * sizeof(K)))
+                             "r"(smem_u32(Y + m0)), "r"((uint32_t)((m1 - m0) * sizeof(K)))
                              : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             if (tid < E) {
                 const int pp = sh + tid;
-                if (pp < m0 && pp < end) g[pp] = so[pp];
+                if (pp < m0 && pp < end) g[pp] = Y[pp];
             } else if (tid < 2 * E) {
                 const int pp = m1 + tid - E;
-                if (pp < end) g[pp] = so[pp];
+                if (pp < end) g[pp] = Y[pp];
             }
         } else {
-            for (int pp = sh + tid; pp < end; pp += NC) g[pp] = so[pp];
+            for (int pp = sh + tid; pp < end; pp += NC) g[pp] = Y[pp];
         }
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
