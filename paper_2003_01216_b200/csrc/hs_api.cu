@@ -152,13 +152,11 @@ struct Workspace {
     uint32_t *sbtab = nullptr;           // K5a split table (sub-range starts) and cursors
     uint32_t *sbcur = nullptr;
     uint16_t *etab = nullptr;            // fine-bin prefixes of tree-bucket pieces (k_tree.cu)
-    void *seg = nullptr;                 // tree plan segments
     size_t zero_bytes = 0;
 };
 
 hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
-                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0, size_t etab_bytes = 0,
-                     size_t seg_bytes = 0) {
+                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0, size_t etab_bytes = 0) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
@@ -167,8 +165,8 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     size_t k = round_up(corank_words * 4, 256);
     size_t sp = round_up(samp_bytes, 256);
     size_t sw = round_up(split_words * 4, 256);
-    size_t eb = round_up(etab_bytes, 256), gb = round_up(seg_bytes, 256);
-    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw + eb + gb;
+    size_t eb = round_up(etab_bytes, 256);
+    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw + eb;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -192,7 +190,6 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
         w->sbcur = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp + sw);
     }
     if (etab_bytes) w->etab = (uint16_t *)(b + a + c + z + th + tp + k + 2 * sp + 2 * sw);
-    if (seg_bytes) w->seg = b + a + c + z + th + tp + k + 2 * sp + 2 * sw + eb;
     w->zero_bytes = c + z;
     return HS_OK;
 }
@@ -477,11 +474,10 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     // on-chip chunk tree (k_tree.cu) for split buckets with an odd number of rounds <= kTreeMaxLog2C
     const bool tree_on = split_on && (log2c & 1) && log2c <= hs::kTreeMaxLog2C;
     const long long max_tiles = tile_bound(n, chunks_per_bucket, T);
-    const long long seg_cap = tree_on ? hs::tree_seg_capacity(dt, n, split_words) : 0;
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
                       (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words,
-                      tree_on ? hs::tree_etab_bytes(max_tiles) : 0, (size_t)seg_cap * 8)) != HS_OK)
+                      tree_on ? hs::tree_etab_bytes(max_tiles) : 0)) != HS_OK)
         return s;
     const hs::Plan *plan = &ws.ctl->plan;
     if (inspect) {  // hs_sort_plan: partition + split into scratch, read the plan back
@@ -498,7 +494,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
             e2 = hs::launch_tile_sort(dt, plan, ws.S, F, ws.S, ws.samp[0], max_tiles, stream, ws.sbtab, &ws.ctl->split,
                                       F, ws.etab);
         if (e2 == cudaSuccess && tree_on)
-            e2 = hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.seg, seg_cap, ws.S, F, stream, true);
+            e2 = hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.S, F, stream, true);
         if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
         if (e2 == cudaSuccess && inspect_treebad)
             e2 = cudaMemcpyAsync(inspect_treebad, &ws.ctl->treebad, sizeof(unsigned), cudaMemcpyDeviceToHost, stream);
@@ -533,7 +529,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                 "K5 tile sort");
     // a6 on chip for tree buckets (S -> keys in one pass)
     if (tree_on)
-        HS_TRY_CUDA(hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.seg, seg_cap, ws.S, keys, stream), "K6t tree");
+        HS_TRY_CUDA(hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.S, keys, stream), "K6t tree");
     // a5 (in-chunk levels) + a6 (tree merge of chunks) of the other buckets: ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
     for (int lv = 0; lv < L; ++lv) {

@@ -279,8 +279,8 @@ struct Ctl {
     unsigned long long hist[10];
     unsigned int done;
     unsigned int ticket;
-    unsigned int treebad;  // tree buckets with a segment over capacity (run merge levels instead)
-    unsigned int nseg;     // segments in the tree plan
+    unsigned int treebad;  // tree buckets with a key segment over capacity (run merge levels instead)
+    unsigned int pad_;
     long long off[11];
     Plan plan;
     SplitCfg split;

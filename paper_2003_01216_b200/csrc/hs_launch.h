@@ -68,13 +68,13 @@ cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const
                                const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st,
                                const unsigned *treebad = nullptr);
 
-// The chunk tree of tree buckets on chip (k_tree.cu): the tree plan cuts every
-// sub-range into key segments from the pieces' fine-bin prefixes (etab), the
-// tree merge runs all log2 c rounds of each segment in shared memory, S -> F.
-long long tree_seg_capacity(int dt, long long n, long long split_words);
+// The chunk tree of tree buckets on chip (k_tree.cu): a check of every key
+// segment's size (over capacity: the bucket falls back to its merge levels),
+// then the tree merge runs all log2 c rounds of each segment in shared memory,
+// S -> F.  etab: the pieces' fine-bin prefixes written by the tile sort.
 size_t tree_etab_bytes(long long max_tiles);
-cudaError_t launch_tree(int dt, Ctl *ctl, const uint32_t *sbtab, const uint16_t *etab, void *seg, long long seg_cap,
-                        const void *S, void *F, cudaStream_t st, bool plan_only = false);
+cudaError_t launch_tree(int dt, Ctl *ctl, const uint32_t *sbtab, const uint16_t *etab, const void *S, void *F,
+                        cudaStream_t st, bool check_only = false);
 // samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);

@@ -73,10 +73,10 @@ def test_tree_even_rounds_keep_the_levels(c):
 
 
 def test_tree_heavy_duplicates_fall_back_per_bucket():
-    """Bucket 3: 70% of its keys are 400 values with ~2.6k copies each (~330 per chunk, so every
-    sub-range piece still fits a tile) -- a fine bin then holds more copies than a tree segment
-    can take, the tree plan marks the bucket and its merge levels run instead; the other
-    buckets keep the on-chip tree.  Both exact."""
+    """Bucket 3: 70% of its keys are 100 values with ~4.6k copies each (~570 per chunk, so every
+    sub-range piece still fits a tile) -- some key segment of 32 fine bins then holds more keys
+    than the tree merge takes, the tree check marks the bucket and its merge levels run instead;
+    the other buckets keep the on-chip tree.  Both exact."""
     T = hs.tile_keys(0, 1)
     c = 8
     m = 3 * T * c
@@ -85,8 +85,8 @@ def test_tree_heavy_duplicates_fall_back_per_bucket():
     parts = []
     for b in range(10):
         if b == 3:
-            vals = rng.integers(3 * div, 4 * div, size=400)
-            dup = vals[rng.integers(0, 400, size=int(0.7 * m))]
+            vals = rng.integers(3 * div, 4 * div, size=100)
+            dup = vals[rng.integers(0, 100, size=int(0.7 * m))]
             parts.append(np.concatenate([dup, rng.integers(3 * div, 4 * div, size=m - dup.size)]))
         else:
             parts.append(rng.integers(b * div, (b + 1) * div, size=m))
