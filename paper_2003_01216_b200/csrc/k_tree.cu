@@ -44,7 +44,8 @@ namespace hs {
 constexpr int kTreeSegBins = 32;                           // bins per segment
 constexpr int kTreeSegs = kTreeFine / kTreeSegBins;        // segments per sub-range
 constexpr int kTreeMaxC = 1 << kTreeMaxLog2C;
-constexpr int kTreeNC = 4 * kTreeSegBins;                  // consumer threads: (pairs x bins x parts) = 4 NB
+constexpr int kTreeLog2TPB = 3;                            // consumer threads per bin: 8
+constexpr int kTreeNC = kTreeSegBins << kTreeLog2TPB;      // consumer threads = (pairs x bins x parts) per round
 constexpr int kTreeST = 2;                                 // stage slots
 
 template <typename K>
@@ -54,8 +55,8 @@ struct TreeSmem {
     static constexpr int E = 16 / sizeof(K);
     // a slot holds the c slices' 16-byte aligned supersets (each <= len + 2E - 2 keys, rounded to E),
     // later the odd rounds' output; Y the even rounds' (+ the destination's 16-byte phase)
-    static constexpr int SLOT = CAP + 2 * E * kTreeMaxC + E;
-    static constexpr int BUF = CAP + 2 * E;
+    static constexpr int SLOT = CAP + 3 * E * kTreeMaxC + E;  // (+ E per slice: its sentinel)
+    static constexpr int BUF = CAP + kTreeMaxC + 2 * E;
     static constexpr size_t bytes() { return (size_t)(kTreeST * SLOT + BUF) * sizeof(K); }
 };
 
@@ -164,11 +165,16 @@ __device__ __forceinline__ void tsts<int64_t>(uint32_t a, int64_t v) {
 
 // Outputs [d0, d1) of the stable-left merge of A[0, na) and B[0, nb) (shared
 // addresses ua, ub) to shared address uo + d0 s: merge-path split of d0, then
-// a serial merge with explicit run ends (keys may equal the dtype maximum).
+// a serial merge.  The element just past each part is >= every key of the
+// other part: the next bin's first key (bins are disjoint key intervals), or
+// the kMax sentinel after a run.  So B is never taken past its end (taken
+// only when strictly smaller), and A's pointer is clamped at its end (a real
+// kMax key in B ties the sentinel: A's kMax is emitted, the same value) --
+// no bounds tests.
 template <typename K>
 __device__ __forceinline__ void tree_merge_part(uint32_t ua, int na, uint32_t ub, int nb, int d0, int d1,
                                                 uint32_t uo) {
-    constexpr int W = sizeof(K);
+    constexpr uint32_t W = sizeof(K);
     int l = d0 - nb > 0 ? d0 - nb : 0;
     int r = d0 < na ? d0 : na;
     while (l < r) {
@@ -178,19 +184,27 @@ __device__ __forceinline__ void tree_merge_part(uint32_t ua, int na, uint32_t ub
         r = pr ? r : mid;
     }
     uint32_t pa = ua + l * W, pb = ub + (d0 - l) * W;
-    const uint32_t ea = ua + na * W, eb = ub + nb * W;
-    K x = tlds<K>(pa), y = tlds<K>(pb);  // (one past a run end stays inside the buffer; masked below)
+    const uint32_t ea = ua + na * W;
+    K x = tlds<K>(pa), y = tlds<K>(pb);
     uint32_t o = uo + d0 * W;
-    const uint32_t oe = uo + d1 * W;
-    for (; o < oe; o += W) {
-        const bool tA = pb >= eb || (pa < ea && x <= y);
+    int cnt = d1 - d0;
+    auto step = [&]() {
+        const bool tA = x <= y;
         tsts<K>(o, tA ? x : y);
-        pa += tA ? W : 0;
-        pb += tA ? 0 : W;
+        o += W;
+        pa = tA ? min(pa + W, ea) : pa;
+        pb += tA ? 0u : W;
         const K t = tlds<K>(tA ? pa : pb);
         x = tA ? t : x;
         y = tA ? y : t;
+    };
+    for (; cnt >= 4; cnt -= 4) {
+        step();
+        step();
+        step();
+        step();
     }
+    for (; cnt > 0; --cnt) step();
 }
 
 // Persistent, warp-specialised; CTA blk owns the contiguous segment range
@@ -292,28 +306,31 @@ __global__ void __launch_bounds__(kTreeNC + 32, 2) k_tree_merge(const Ctl *__res
             const uintptr_t ga0 = (uintptr_t)src & ~(uintptr_t)15;
             const uintptr_t ga1 = ((uintptr_t)(src + len) + 15) & ~(uintptr_t)15;
             const int words = len > 0 ? (int)((ga1 - ga0) / W) : 0;  // multiple of E
-            int incl = words;
+            int incl = lane < c ? words + E : 0;  // + a gap for the sentinel after the slice
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
-            const int region = incl - words;
+            const int region = incl - (lane < c ? words + E : 0);
             int M = len, outsum = outpart;
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) {
                 M += __shfl_xor_sync(0xffffffffu, M, o);
                 outsum += __shfl_xor_sync(0xffffffffu, outsum, o);
             }
-            const int total_words = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane < c) d.off[lane] = region + (int)(((uintptr_t)src - ga0) / W);
+            const int total_words = __shfl_sync(0xffffffffu, incl, 31);  // (incl. gaps)
+            int tx = words;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+            if (lane < c) d.off[lane] = len > 0 ? region + (int)(((uintptr_t)src - ga0) / W) : region;
             if (lane == 0) {
                 d.M = M;
                 d.out = P.off[b] + outsum;
             }
             HS_DASSERT(M <= G::CAP && total_words <= SLOT);
             __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)total_words * W);
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)tx * W);
             __syncwarp();
             if (words > 0) bulk_g2s(stage0 + slot * SLOT + region, (const void *)ga0, (uint32_t)words * W, &full[slot]);
             ++it;
@@ -333,13 +350,14 @@ __global__ void __launch_bounds__(kTreeNC + 32, 2) k_tree_merge(const Ctl *__res
         K *const out = F + d.out;
         const int sh = (int)(((uintptr_t)out & 15) / W);
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // Y free again
+        if (tid < c) sb[d.off[tid] + d.T[tid][NB]] = KeyTraits<K>::kMax;  // sentinel after each slice
         tree_bar();
         for (int r = 0; r < lg; ++r) {
             const bool last = r + 1 == lg;
             const int m = 1 << r;                 // pieces per input run
-            const int npairs = c >> (r + 1);
-            const int S_ = NC / (npairs * NB);    // threads per (pair, bin) unit
-            const int unit = tid / S_, part = tid % S_;
+            // threads per (pair, bin) unit: S_ = NC / (pairs NB) = 2^lS (pairs = c >> (r + 1))
+            const int lS = kTreeLog2TPB - lg + r + 1;
+            const int unit = tid >> lS, part = tid & ((1 << lS) - 1);
             const int q = unit / NB, u = unit % NB;
             // bin u / u + 1 starts of runs 2q (A: pieces [2qm, 2qm + m)) and 2q + 1 (B); the pieces
             // before 2qm give the pair's base in the round's buffers
@@ -358,14 +376,21 @@ __global__ void __launch_bounds__(kTreeNC + 32, 2) k_tree_merge(const Ctl *__res
             if (r == 0) {  // the stage slices
                 ua = usb + (d.off[2 * q] + a_u) * W;
                 ub = usb + (d.off[2 * q + 1] + b_u) * W;
-            } else {       // the previous round's buffer: runs contiguous from its start
+            } else {       // the previous round's buffer: run k at (pieces before it) + k (one sentinel each)
                 const uint32_t in = (r & 1) ? uY : usb;
-                ua = in + (before + a_u) * W;
-                ub = in + (before + la_tot + b_u) * W;
+                ua = in + (before + 2 * q + a_u) * W;
+                ub = in + (before + la_tot + 2 * q + 1 + b_u) * W;
             }
             const int na = a_u1 - a_u, nb = b_u1 - b_u, n = na + nb;
-            const uint32_t uo = ((r & 1) ? usb : uY + (last ? sh : 0) * W) + (before + a_u + b_u) * W;
-            tree_merge_part<K>(ua, na, ub, nb, n * part / S_, n * (part + 1) / S_, uo);
+            K *const ob = (r & 1) ? sb : Y + (last ? sh : 0);
+            const int obase = last ? 0 : before + q;  // pair q's output run, after q sentinels
+            tree_merge_part<K>(ua, na, ub, nb, (n * part) >> lS, (n * (part + 1)) >> lS,
+                               smem_u32(ob) + (obase + a_u + b_u) * W);
+            if (!last && u == NB - 1 && part == 0) {  // the sentinel after pair q's output run
+                int lb_tot = 0;
+                for (int j = 2 * q * m + m; j < 2 * q * m + 2 * m; ++j) lb_tot += d.T[j][NB];
+                ob[obase + la_tot + lb_tot] = KeyTraits<K>::kMax;
+            }
             tree_bar();  // round complete
         }
         if ((tid & 31) == 0) tree_arrive(&empty[slot]);  // the slot (inputs and odd rounds) is free
