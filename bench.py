@@ -324,10 +324,9 @@ def run_ours(args, cfg):
         off_h = off.cpu().numpy()
     levels, tile_levels = hs.plan_levels(off_h, 1 if pairs else dt_code, cfg.chunks, 0)
     split = [0] * 10
-    tree = [0] * 10
-    if not shared and not pairs:  # the device plan: which buckets the K5a value split took, which run the chunk tree on chip
+    if not shared and not pairs:  # the device plan: which buckets the K5a value split took
         dplan = hs.hs_sort_plan(src, cfg.num_digits, cfg.chunks)
-        levels, split, tree = dplan["levels"], dplan["split"], dplan["tree"]
+        levels, split = dplan["levels"], dplan["split"]
     if pairs:
         ksize = 8  # the items (key << 32 | index) travel through the int64 path
     m = np.diff(off_h)
@@ -337,14 +336,11 @@ def run_ours(args, cfg):
             per_kernel[kind] = {"ms_per_step": tot / args.steps, "launches_per_step": cnt // args.steps}
     dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"])
     L_launch = per_kernel.get("merge_level", {}).get("launches_per_step", 0)
-    level_bytes = [2 * ksize * int(sum(m[b] for b in range(10) if levels[b] > lv and not tree[b]))
-                   for lv in range(L_launch)]
+    level_bytes = [2 * ksize * int(sum(m[b] for b in range(10) if levels[b] > lv)) for lv in range(L_launch)]
     m_split = int(sum(m[b] for b in range(10) if split[b]))
-    m_tree = int(sum(m[b] for b in range(10) if tree[b]))
     alg = {  # algorithmic bytes per step of each kernel kind
         "tile_hist": ksize * cfg.n, "scatter": 2 * ksize * cfg.n, "tile_sort": 2 * ksize * cfg.n,
         "merge_level": sum(level_bytes), "split_count": ksize * m_split, "split_scatter": 2 * ksize * m_split,
-        "tree_merge": 2 * ksize * m_tree,
     }
     for k, d in per_kernel.items():
         if k in alg and d["ms_per_step"] > 0:
@@ -362,15 +358,14 @@ def run_ours(args, cfg):
                 "alg_bytes_per_launch": (statistics.mean(active) if dom == "merge_level" and active else alg.get(dom)),
                 "launches_per_step": per_kernel[dom]["launches_per_step"],
                 "active_launches_per_step": len(active) if dom == "merge_level" else 1}
-    # hist r + scatter r/w (MSD path only) + K5a split count r + scatter r/w (split buckets) + tile sort r/w
-    # + merge levels + the on-chip chunk tree (one r/w pass of its buckets)
-    path_bytes = ksize * cfg.n * (2 if shared else 5) + 3 * ksize * m_split + sum(level_bytes) + 2 * ksize * m_tree
+    # hist r + scatter r/w (MSD path only) + K5a split count r + scatter r/w (split buckets) + tile sort r/w + merge levels
+    path_bytes = ksize * cfg.n * (2 if shared else 5) + 3 * ksize * m_split + sum(level_bytes)
     if pairs:  # pack (r 4 + w 8), tag copy (r 8 + w 8), unpack (r 8 + tag gather 8 + w 4 + w 8)
         path_bytes += cfg.n * (12 + 16 + 28)
     step_roof = {"alg_bytes_per_step": path_bytes, "bytes_per_key": path_bytes / cfg.n,
                  "t_roof_ms": path_bytes / (peak * 1e9) * 1e3,
                  "frac": path_bytes / (peak * 1e9) / (ms * 1e-3), "levels": max(levels),
-                 "split_buckets": int(sum(split)), "tree_buckets": int(sum(tree))}
+                 "split_buckets": int(sum(split))}
 
     # ---- end to end through the public API with pinned host buffers
     e2e_ms = []

@@ -298,13 +298,9 @@ hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_dig
  * K5a value split takes, hence how many merge levels run).  Runs the
  * partition and the split into scratch memory (keys is not modified),
  * synchronises the stream and writes, per bucket b (host arrays of 10):
- * levels_out[b] = merge levels L[b] of the plan, split_out[b] = 1 if bucket
- * b's chunks were value-split and 2 if, in addition, its chunk tree (the
- * log2 c merge rounds) runs on chip in one HBM pass (equal-width
- * sub-ranges, odd log2 c <= 5, no key segment over capacity; k_tree.cu),
- * leaves_out[b] = tile-sort leaves per chunk.  For tree buckets it also runs
- * the tile sort and the tree plan into scratch.  Arguments and errors as
- * hs_sort.
+ * levels_out[b] = merge levels L[b], split_out[b] = 1 if bucket b's chunks
+ * were value-split, leaves_out[b] = tile-sort leaves per chunk.  Arguments
+ * and errors as hs_sort.
  */
 hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                          int32_t *levels_out, int32_t *split_out, int32_t *leaves_out, cudaStream_t stream);

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "hs_sort_buckets",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy",
-                 "split_count", "split_scatter", "tree_plan", "tree_merge")
+                 "split_count", "split_scatter")
 
 
 class HybridSortError(RuntimeError):
@@ -294,9 +294,7 @@ def hs_sort_buckets(keys, bucket_offsets, num_digits: int, chunks_per_bucket: in
 
 def hs_sort_plan(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None):
     """The plan hs_sort would run on keys (keys unchanged): dict of per-bucket
-    merge levels, K5a split flags, tile-sort leaves per chunk, and whether the
-    bucket's chunk tree is eligible to run on chip in one pass (k_tree.cu;
-    a bucket with a key segment over capacity still falls back to its levels)."""
+    merge levels, K5a split flags and tile-sort leaves per chunk."""
     import numpy as np
     torch = _torch()
     _check_tensor(keys, "keys")
@@ -307,8 +305,7 @@ def hs_sort_plan(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None)
     with torch.cuda.device(keys.device):
         _check(load().hs_sort_plan(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket,
                                    L.ctypes.data, sp.ctypes.data, lv.ctypes.data, _stream(stream)))
-    return {"levels": L.tolist(), "split": [min(int(v), 1) for v in sp], "leaves": lv.tolist(),
-            "tree": [int(v == 2) for v in sp]}
+    return {"levels": L.tolist(), "split": sp.tolist(), "leaves": lv.tolist()}
 
 
 def hs_sort_shared(keys, chunks: int = 8, stream=None):

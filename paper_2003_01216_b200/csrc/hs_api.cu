@@ -67,7 +67,6 @@ cudaError_t device_setup(int *num_sms) {
         if (err == cudaSuccess) err = hs::setup_tilesort_kernels(dev);
         if (err == cudaSuccess) err = hs::setup_merge_kernels(dev);
         if (err == cudaSuccess) err = hs::setup_split_kernels(dev);
-        if (err == cudaSuccess) err = hs::setup_tree_kernels(dev);
     });
     if (err != cudaSuccess) return err;
     *num_sms = g_num_sms[dev];
@@ -151,12 +150,11 @@ struct Workspace {
     void *samp[2] = {nullptr, nullptr};  // key samples (ping-pong by merge level)
     uint32_t *sbtab = nullptr;           // K5a split table (sub-range starts) and cursors
     uint32_t *sbcur = nullptr;
-    uint16_t *etab = nullptr;            // fine-bin prefixes of tree-bucket pieces (k_tree.cu)
     size_t zero_bytes = 0;
 };
 
 hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
-                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0, size_t etab_bytes = 0) {
+                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
@@ -165,8 +163,7 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     size_t k = round_up(corank_words * 4, 256);
     size_t sp = round_up(samp_bytes, 256);
     size_t sw = round_up(split_words * 4, 256);
-    size_t eb = round_up(etab_bytes, 256);
-    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw + eb;
+    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -189,7 +186,6 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
         w->sbtab = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp);
         w->sbcur = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp + sw);
     }
-    if (etab_bytes) w->etab = (uint16_t *)(b + a + c + z + th + tp + k + 2 * sp + 2 * sw);
     w->zero_bytes = c + z;
     return HS_OK;
 }
@@ -256,9 +252,9 @@ cudaEvent_t prof_event() {
     return e;
 }
 
-const char *const kProfNames[hs::kProfKinds] = {"tile_hist",     "tile_scan",  "scatter",       "plan",
-                                                 "tile_sort",     "merge_partition", "merge_level", "copy",
-                                                 "split_count",   "split_scatter",   "tree_plan",   "tree_merge"};
+const char *const kProfNames[hs::kProfKinds] = {"tile_hist", "tile_scan", "scatter", "plan",
+                                                 "tile_sort", "merge_partition", "merge_level", "copy",
+                                                 "split_count", "split_scatter"};
 
 }  // namespace
 
@@ -453,7 +449,7 @@ namespace {
 // digit into those buckets -- a1-a3 are skipped, the plan comes from user_off,
 // the split reads keys and writes the scratch, the tile sort reads both.
 hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
-                      int log2c, cudaStream_t stream, hs::Plan *inspect = nullptr, unsigned *inspect_treebad = nullptr,
+                      int log2c, cudaStream_t stream, hs::Plan *inspect = nullptr,
                       const int64_t *user_off = nullptr) {
     hs_status_t s;
     int sms;
@@ -471,15 +467,10 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     // K5a value split of the chunks (compile-time HS_SPLIT, see the top of this file)
     constexpr bool split_on = HS_SPLIT != 0;
     const long long split_words = split_on ? hs::split_table_words(n, log2c, T) : 0;
-    // on-chip chunk tree (k_tree.cu) for split buckets with an odd number of rounds <= kTreeMaxLog2C
-    const bool tree_on = split_on && (log2c & 1) && log2c <= hs::kTreeMaxLog2C;
-    const long long max_tiles = tile_bound(n, chunks_per_bucket, T);
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
-                      (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words,
-                      tree_on ? hs::tree_etab_bytes(max_tiles) : 0)) != HS_OK)
+                      (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words)) != HS_OK)
         return s;
-    const hs::Plan *plan = &ws.ctl->plan;
     if (inspect) {  // hs_sort_plan: partition + split into scratch, read the plan back
         void *F = (char *)ws.S + round_up((size_t)n * ksize(dtype), 256);
         cudaError_t e2 = cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream);
@@ -489,21 +480,14 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         if (e2 == cudaSuccess && split_on)
             e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
                                   stream);
-        // tree buckets: tile sort (scratch only) + tree plan, to learn which ones fall back to merge levels
-        if (e2 == cudaSuccess && tree_on)
-            e2 = hs::launch_tile_sort(dt, plan, ws.S, F, ws.S, ws.samp[0], max_tiles, stream, ws.sbtab, &ws.ctl->split,
-                                      F, ws.etab);
-        if (e2 == cudaSuccess && tree_on)
-            e2 = hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.S, F, stream, true);
         if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
-        if (e2 == cudaSuccess && inspect_treebad)
-            e2 = cudaMemcpyAsync(inspect_treebad, &ws.ctl->treebad, sizeof(unsigned), cudaMemcpyDeviceToHost, stream);
         cudaError_t fe = cudaFreeAsync(ws.base, stream);
         if (e2 == cudaSuccess) e2 = fe;
         if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(stream);
         if (e2 != cudaSuccess) return cuda_fail(e2, "hs_sort_plan");
         return HS_OK;
     }
+    const hs::Plan *plan = &ws.ctl->plan;
     HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
     // where the partitioned keys are (part) and where the split writes (spl)
     void *part = ws.S, *spl = keys;
@@ -524,18 +508,14 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                                      key_shift, stream),
                     "K5a split");
     // a5: leaf-tile sort (part, or spl for split buckets) -> (keys | S) per bucket parity
-    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], max_tiles, stream, ws.sbtab,
-                                     &ws.ctl->split, spl, ws.etab),
+    HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
+                                     ws.sbtab, &ws.ctl->split, spl),
                 "K5 tile sort");
-    // a6 on chip for tree buckets (S -> keys in one pass)
-    if (tree_on)
-        HS_TRY_CUDA(hs::launch_tree(dt, ws.ctl, ws.sbtab, ws.etab, ws.S, keys, stream), "K6t tree");
-    // a5 (in-chunk levels) + a6 (tree merge of chunks) of the other buckets: ping-pong, last level lands in keys
+    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);
     for (int lv = 0; lv < L; ++lv) {
         HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
-                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream,
-                                           tree_on ? &ws.ctl->treebad : nullptr),
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
                     "K6 merge level");
     }
     cudaError_t fe = cudaFreeAsync(ws.base, stream);
@@ -582,8 +562,7 @@ hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_dig
         return HS_OK;
     }
     g_launch_counter = 0;
-    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, nullptr, nullptr,
-                       bucket_offsets)) !=
+    if ((s = sort_impl(keys, n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, nullptr, bucket_offsets)) !=
         HS_OK)
         return s;
     return succeed();
@@ -600,17 +579,15 @@ hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_
     if (!levels_out || !split_out || !leaves_out) return fail(HS_ERR_INVALID_VALUE, "output array is NULL");
     hs::Plan P;
     memset(&P, 0, sizeof(P));
-    unsigned treebad = 0;
     if (n > 0) {
         g_launch_counter = 0;
-        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &P,
-                           &treebad)) != HS_OK)
+        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &P)) !=
+            HS_OK)
             return s;
     }
     for (int b = 0; b < 10; ++b) {
-        // 2: split, and the chunk tree runs on chip (k_tree.cu); 1: split, chunk tree as merge levels
-        split_out[b] = P.split[b] + (P.tree[b] && !((treebad >> b) & 1u));
-        levels_out[b] = n > 0 ? P.L[b] : 0;  // (a tree bucket runs them as one on-chip pass)
+        levels_out[b] = n > 0 ? P.L[b] : 0;
+        split_out[b] = P.split[b];
         leaves_out[b] = P.split[b] ? P.nsb[b] : (1 << P.k[b]);
     }
     g_launches = 0;

@@ -117,12 +117,6 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 //    value into nsb[b] sub-ranges, each at most T keys; the tile-sort leaves
 //    are those sub-ranges (bounds in the split table at sboff[b]), k[b] = 0
 //    and the merge levels are only the paper's chunk tree (L[b] = log2 c).
-//  * tree[b] = 1 (a split bucket with equal-width sub-ranges and c = 2 or 8,
-//    k_tree.cu): sub-range t covers the same key interval in
-//    every chunk, so the chunk tree of the bucket is run per (sub-range, key
-//    segment) on chip -- all log2 c rounds in one HBM pass -- unless the tree
-//    plan finds a segment over capacity (ctl->treebad), in which case the
-//    bucket runs its L[b] merge levels as usual (same buffers: L[b] is odd).
 struct Plan {
     long long off[11];
     long long tile_prefix[11];  // exclusive prefix of tile-sort leaf counts (c << k[b], or c * nsb[b])
@@ -131,16 +125,9 @@ struct Plan {
     int L[10];
     int split[10];
     int nsb[10];
-    int tree[10];
     int log2c;
     int Lmax;
 };
-
-// Tree map of the on-chip chunk tree (k_tree.cu): the key interval of an
-// equal-width sub-range is cut into kTreeFine equal fine bins; the tile sort
-// of every piece records e[u] = #keys of the piece in bins <= u.
-constexpr int kTreeFineLog2 = 10, kTreeFine = 1 << kTreeFineLog2;
-constexpr int kTreeMaxLog2C = 3;  // c <= 8: the tree merge's shared-memory layout
 
 // K5a bookkeeping (value split of the chunks), written by k_split_setup and
 // k_split_map.  Fine bins: kSplitFine equal-width bins of a bucket's digit
@@ -188,7 +175,6 @@ __device__ inline void compute_plan(Plan *P, const long long *off, int log2c, in
         int L = (mode == kPlanSort) ? k + log2c : (mode == kPlanChunks ? k : log2c);
         P->off[b] = off[b];
         P->split[b] = 0;
-        P->tree[b] = 0;
         P->nsb[b] = 0;
         P->sboff[b] = 0;
         P->k[b] = k;
@@ -279,8 +265,6 @@ struct Ctl {
     unsigned long long hist[10];
     unsigned int done;
     unsigned int ticket;
-    unsigned int treebad;  // tree buckets with a key segment over capacity (run merge levels instead)
-    unsigned int pad_;
     long long off[11];
     Plan plan;
     SplitCfg split;

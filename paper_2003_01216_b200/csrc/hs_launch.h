@@ -14,8 +14,7 @@ struct Plan;
 // Optional per-kernel CUDA-event timing (hs_profile_enable); kinds match
 // hs_profile_kind_name().  No-ops unless enabled on the calling thread.
 enum ProfKind { kProfTileHist = 0, kProfTileScan, kProfScatter, kProfPlan, kProfTileSort, kProfMergePartition,
-                kProfMergeLevel, kProfCopy, kProfSplitCount, kProfSplitScatter, kProfTreePlan, kProfTreeMerge,
-                kProfKinds };
+                kProfMergeLevel, kProfCopy, kProfSplitCount, kProfSplitScatter, kProfKinds };
 void prof_begin(int kind, cudaStream_t st);
 void prof_end(int kind, cudaStream_t st);
 // Kernel launch accounting (hs_last_launch_count): every successful kernel
@@ -30,7 +29,6 @@ cudaError_t setup_partition_kernels(int dev);
 cudaError_t setup_tilesort_kernels(int dev);
 cudaError_t setup_merge_kernels(int dev);
 cudaError_t setup_split_kernels(int dev);
-cudaError_t setup_tree_kernels(int dev);
 
 int scatter_tile_keys(int dt);  // keys per K1/K3 tile
 int sort_tile_keys(int dt);     // leaf-tile capacity T of K5
@@ -47,11 +45,9 @@ cudaError_t launch_plan(const long long *user_off, Ctl *ctl, int log2c, int mode
 cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, cudaStream_t st);  // one segment
 // sbtab: K5a split table (leaves of split buckets; null when no bucket can be split)
 struct SplitCfg;
-// etab: fine-bin prefixes of the pieces of tree buckets (k_tree.cu; null: none recorded)
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr,
-                             const SplitCfg *scfg = nullptr, const void *src_split = nullptr,  // null: F
-                             uint16_t *etab = nullptr);
+                             const SplitCfg *scfg = nullptr, const void *src_split = nullptr);  // null: F
 
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +
@@ -62,19 +58,9 @@ cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab
                          long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
                          cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
-// the samples this level writes for the next one (may be null).  treebad
-// (may be null): buckets with plan.tree set are skipped unless their bit is set.
+// the samples this level writes for the next one (may be null).
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
-                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st,
-                               const unsigned *treebad = nullptr);
-
-// The chunk tree of tree buckets on chip (k_tree.cu): a check of every key
-// segment's size (over capacity: the bucket falls back to its merge levels),
-// then the tree merge runs all log2 c rounds of each segment in shared memory,
-// S -> F.  etab: the pieces' fine-bin prefixes written by the tile sort.
-size_t tree_etab_bytes(long long max_tiles);
-cudaError_t launch_tree(int dt, Ctl *ctl, const uint32_t *sbtab, const uint16_t *etab, const void *S, void *F,
-                        cudaStream_t st, bool check_only = false);
+                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st);
 // samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);

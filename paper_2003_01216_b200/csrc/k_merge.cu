@@ -80,34 +80,14 @@ __device__ __forceinline__ void load_plan_m(Plan &dst, const Plan *src) {
 //     surely true, surely false or open; two binary searches over these
 //     candidates (samples only: L2-resident) leave an interval of ~Q keys;
 //   fine: plain binary search of Q(m) over that interval (the only HBM reads).
-// Bucket b runs merge level `level` unless it has no such level or its chunk
-// tree ran on chip (k_tree.cu: plan.tree set and no over-capacity segment).
-__device__ __forceinline__ bool level_active(const Plan &P, int b, int level, unsigned tbad) {
-    return level < P.L[b] && !(P.tree[b] && !((tbad >> b) & 1u));
-}
-
-// Does any bucket run this level?  (Read straight from the global plan, so a
-// launch past the device plan -- the host only knows a bound -- exits at once.)
-__device__ __forceinline__ bool level_any(const Plan *__restrict__ g, int level, const unsigned *treebad) {
-    if (level >= __ldg(&g->Lmax)) return false;
-    const unsigned tbad = treebad ? *treebad : ~0u;
-    bool any = false;
-#pragma unroll
-    for (int b = 0; b < 10; ++b)
-        any |= level < __ldg(&g->L[b]) && !(__ldg(&g->tree[b]) && !((tbad >> b) & 1u));
-    return any;
-}
-
 template <typename K>
 __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
-                                  const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds,
-                                  const unsigned *treebad) {
+                                  const K *__restrict__ samp, int *corank, int level, int n, int TM, int nbounds) {
     constexpr long long Q = kSampleQ;
     griddep_wait();
-    if (!level_any(plan_g, level, treebad)) return;  // no bucket runs this level (the host only knows a bound)
+    if (level >= __ldg(&plan_g->Lmax)) return;  // no bucket runs this level (the host only knows a bound)
     __shared__ Plan P;
     load_plan_m(P, plan_g);
-    const unsigned tbad = treebad ? *treebad : ~0u;
     __syncthreads();
     if (level >= P.Lmax) return;  // no bucket runs this level (the host only knows a bound)
     const int beta = blockIdx.x * blockDim.x + threadIdx.x;
@@ -115,7 +95,7 @@ __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, c
     const long long x = (long long)beta * TM;
     if (x >= n) return;
     const int b = bucket_of(P, x);
-    if (!level_active(P, b, level, tbad)) return;
+    if (level >= P.L[b]) return;
     const PairGeom g = pair_of(P, b, leaf_of(P, b, x), level);
     const K *src = (level == 0 && src0) ? src0 : level_src(P, b, level, F, S);
     const long long diag = x - g.a_lo;
@@ -220,7 +200,7 @@ __device__ __forceinline__ int merge_path(const K *A, int na, const K *B, int nb
 template <typename K, int NC, int VT, int ST>
 __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict__ plan_g, K *F, K *S, const K *src0,
                                                          const int *__restrict__ corank, K *samp_out, int level,
-                                                         int n, int nblocks, const unsigned *treebad) {
+                                                         int n, int nblocks) {
     using SM = MergeSmem<K, NC, VT, ST>;
     constexpr int TM = SM::TM, E = SM::E, SLOT = SM::SLOT, OUT = SM::OUT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -234,7 +214,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     const K kMax = KeyTraits<K>::kMax;
 
     griddep_wait();
-    if (!level_any(plan_g, level, treebad)) return;  // whole CTA: nothing at this level
+    if (level >= __ldg(&plan_g->Lmax)) return;  // whole CTA: nothing at this level
     load_plan_m(P, plan_g);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
@@ -249,7 +229,6 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     if (tid >= NC) {
         // ------------------------------------------------------ producer
         if (tid != NC) return;
-        const unsigned tbad = treebad ? *treebad : ~0u;
         int blk = blockIdx.x;
         long long px = (long long)blk * TM;
         for (int it = 0;; ++it) {
@@ -266,7 +245,7 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
                     continue;
                 }
                 const int b = bucket_of(P, px);
-                if (!level_active(P, b, level, tbad)) {
+                if (level >= P.L[b]) {
                     px = P.off[b + 1];
                     continue;
                 }
@@ -460,7 +439,7 @@ cudaError_t setup_merge_kernels(int dev) {
 template <typename K>
 cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void *src0, int *corank,
                                  const void *samp_in, void *samp_out, int level, int n, int num_sms,
-                                 cudaStream_t st, const unsigned *treebad) {
+                                 cudaStream_t st) {
     using G = MGeo<K>;
     using SM = MergeSmem<K, G::kNT, G::kVT, G::kST>;
     constexpr int TM = SM::TM;
@@ -487,7 +466,7 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_merge_partition<K>, plan, (K *)F, (K *)S, (const K *)src0,
-                                       (const K *)samp_in, corank, level, n, TM, nbounds, treebad);
+                                       (const K *)samp_in, corank, level, n, TM, nbounds);
     prof_end(kProfMergePartition, st);
     if (e != cudaSuccess) return e;
     note_launch();
@@ -498,7 +477,7 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     cfg.blockDim = dim3(G::kNT + 32);
     cfg.dynamicSmemBytes = SM::bytes();
     e = cudaLaunchKernelEx(&cfg, kern, plan, (K *)F, (K *)S, (const K *)src0, (const int *)corank, (K *)samp_out,
-                           level, n, nblocks, treebad);
+                           level, n, nblocks);
     prof_end(kProfMergeLevel, st);
     if (e != cudaSuccess) return e;
     note_launch();
@@ -533,12 +512,9 @@ cudaError_t launch_copy_t(const void *src, void *dst, long long n, int num_sms, 
 int merge_span(int dt) { return dt == 0 ? merge_span_t<int32_t>() : merge_span_t<int64_t>(); }
 
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
-                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st,
-                               const unsigned *treebad) {
-    return dt == 0 ? launch_merge_level_t<int32_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st,
-                                                   treebad)
-                   : launch_merge_level_t<int64_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st,
-                                                   treebad);
+                               const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st) {
+    return dt == 0 ? launch_merge_level_t<int32_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st)
+                   : launch_merge_level_t<int64_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st);
 }
 
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st) {

@@ -681,9 +681,6 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
     for (int bb = 0; bb < 10; ++bb) {
         const int sp = C.cand[bb] && !((bad >> bb) & 1u);
         P.split[bb] = sp;
-        // equal-width sub-ranges share their key interval across the chunks: the chunk tree can run
-        // on chip (k_tree.cu; odd log2 c keeps the tile sort's output buffer that of the level path)
-        P.tree[bb] = sp && C.mode[bb] == 0 && (lg & 1) && lg <= kTreeMaxLog2C;
         if (sp) {
             P.k[bb] = 0;
             P.L[bb] = lg;  // only the chunk tree (a6) remains

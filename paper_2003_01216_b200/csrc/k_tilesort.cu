@@ -150,49 +150,10 @@ struct TSGeo {
     static constexpr size_t bytes() { return (size_t)(T + 2 * E) * sizeof(K); }
 };
 
-// Fine bin of key k in the tree map of sub-range t of a tree bucket (k_tree.cu):
-// with d = max(x - lo, 0) (x = k >> shift, as K5a's sub-range map), the keys
-// of sub-range t have mulhi(d, mul) = t and the low word of d * mul rises with
-// the key across the sub-range -- its top kTreeFineLog2 bits are the bin, the
-// same function of the key in every chunk.  Keys clamped past the bucket's
-// range (only in its last sub-range) take the last bin; non-decreasing in k.
-__device__ __forceinline__ int tree_bin(int32_t k, int, long long lo, unsigned long long mul, int t) {
-    const uint32_t d = (uint32_t)max(k - (int32_t)lo, 0);
-    const uint32_t hi = __umulhi(d, (uint32_t)mul);
-    if (hi != (uint32_t)t) return hi > (uint32_t)t ? kTreeFine - 1 : 0;
-    return (int)((d * (uint32_t)mul) >> (32 - kTreeFineLog2));
-}
-__device__ __forceinline__ int tree_bin(int64_t k, int shift, long long lo, unsigned long long mul, int t) {
-    const unsigned long long d = (unsigned long long)max((k >> shift) - lo, 0LL);
-    const unsigned long long hi = __umul64hi(d, mul);
-    if (hi != (unsigned long long)t) return hi > (unsigned long long)t ? kTreeFine - 1 : 0;
-    return (int)((d * mul) >> (64 - kTreeFineLog2));
-}
-
-// e[u] = #keys of the sorted piece so[0, len) with tree bin <= u, u < kTreeFine,
-// by binary search (pieces whose bucket pass did not run on the tree bins:
-// edge sub-ranges, narrow ones, tiles that took the merge rounds).  A piece
-// whose bucket pass ran on the fraction bins writes e from its bucket counts
-// instead (they are the same bins).
-template <typename K>
-__device__ __forceinline__ void write_tree_prefix(uint16_t *e, const K *so, int len, long long lo,
-                                                  unsigned long long mul, int shift, int t, int tid, int nthreads) {
-    for (int u = tid; u < kTreeFine; u += nthreads) {
-        int l = 0, r = len;  // first position whose bin exceeds u
-        while (l < r) {
-            const int mid = (l + r) >> 1;
-            if (tree_bin(so[mid], shift, lo, mul, t) <= u) l = mid + 1;
-            else r = mid;
-        }
-        e[u] = (uint16_t)l;
-    }
-}
-
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp, const uint32_t *__restrict__ sbtab,
-                                                        const SplitCfg *__restrict__ scfg, const K *src_split,
-                                                        uint16_t *etab) {
+                                                        const SplitCfg *__restrict__ scfg, const K *src_split) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
@@ -223,7 +184,6 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     bool frac = false;
     U f_base = 0, f_mul = 0;
     int f_sft = 0;
-    int tree_t = -1;  // >= 0: piece of a tree bucket (sub-range tree_t): record its fine-bin prefix
     if (P.split[b]) {  // K5a split this bucket: the leaf is sub-range t of chunk j (in src_split)
         const int ns = P.nsb[b];
         const long long j = (unsigned)i / (unsigned)ns, t = i - j * ns;  // i < c * ns < 2^31
@@ -238,16 +198,11 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
             f_mul = mul;
             f_sft = scfg->shift;
         }
-        if (P.tree[b] && etab) tree_t = (int)t;
     } else {
         lo = leaf_start(P, b, i);
         len = (int)(leaf_start(P, b, i + 1) - lo);
     }
-    if (len == 0) {
-        if (tree_t >= 0)
-            for (int u = tid; u < kTreeFine; u += NT) etab[g * kTreeFine + u] = 0;
-        return;
-    }
+    if (len == 0) return;
     HS_DASSERT(len > 0 && len <= T && lo >= P.off[b] && lo + len <= P.off[b + 1]);
     K *const out = ((P.L[b] & 1) ? S : F) + lo;  // where this bucket's merge level 0 reads
     const K kMax = KeyTraits<K>::kMax;
@@ -557,16 +512,6 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         for (int p = tid; p < len; p += NT) out[p] = so[p];
     }
     write_samples(samp, lo, len, so, tid, NT);  // coarse index for merge level 0's co-rank search
-    if (tree_t >= 0) {
-        uint16_t *const e = etab + g * kTreeFine;
-        if (frac && mode == 2 && BUCKETS == kTreeFine && BPT_ == 2) {
-            // the bucket pass ran on the fraction bins = the tree bins: e from my two buckets' ends
-            const uint32_t e0 = bk_base + bk_cnt[0], e1 = e0 + bk_cnt[BPT_ - 1];
-            reinterpret_cast<uint32_t *>(e)[tid] = e0 | (e1 << 16);
-        } else {
-            write_tree_prefix(e, so, len, scfg->lo[b], scfg->mul[b], scfg->shift, tree_t, tid, NT);
-        }
-    }
 }
 
 // =============================================================== launchers
@@ -619,15 +564,14 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
-                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split,
-                               uint16_t *etab) {
+                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)max_tiles), dim3(G::kNT), smem, st, plan, (const K *)src, (K *)F,
-                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F), etab);
+                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F));
     if (e != cudaSuccess) return e;
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
@@ -635,9 +579,9 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg,
-                             const void *src_split, uint16_t *etab) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, etab)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, etab);
+                             const void *src_split) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split);
 }
 
 }  // namespace hs
