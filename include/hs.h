@@ -193,6 +193,43 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
                           cudaStream_t stream);
 
 /*
+ * SURVEY §8(f) row f3 on the stable item path (k_kv.cu): SPEC's SortItem
+ * (S:31-37), a key plus a 64-bit tag that "never influences order", carried
+ * WITH its key through every pass as a 16-byte item (no gather by index).
+ * Every kernel the items pass through is stable -- the counting scatter of
+ * the MSD step, an odd-even transposition sort of adjacent items plus
+ * stable-left merge rounds inside a tile, and the stable-left merge levels of
+ * the paper's tree merge -- so equal keys keep their input
+ * order ("Merge sort is a stable sort").  No K5a value split on this
+ * path (its atomic ranking is not stable): chunks are sorted as tiles + merge
+ * levels.  Keys of either dtype (int32 widen to the item's int64 key: same
+ * order, same leading digit).  tags / out_tags: device uint64_t[n].
+ *
+ * hs_sort_pairs64: the whole path (a1-a7) on int64 keys, in place.
+ * hs_msd_partition_pairs64: a1-a3 on int64 keys (out of place; outputs must
+ *   not overlap the inputs); bucket_offsets[11] as hs_msd_partition.
+ * hs_sort_chunks_pairs: a5 only -- every chunk (partition_even of each bucket
+ *   of bucket_offsets) sorted stably; in == out allowed.
+ * hs_merge_pairs: a6 only -- the log2 c tree-merge rounds of each bucket's
+ *   chunk-sorted runs on SortItems with a key-only comparator, ties taking the
+ *   left run; in == out allowed.
+ * n < 2^31; num_digits in [1, 19]; chunks_per_bucket a power of two in
+ * [1, 65536]; errors as hs_sort (HS_ERR_INVALID_VALUE also for keys / tags
+ * overlapping).  Scratch: 32 n bytes from the stream-ordered pool.
+ */
+hs_status_t hs_sort_pairs64(int64_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
+                            cudaStream_t stream);
+hs_status_t hs_msd_partition_pairs64(const int64_t *keys, const uint64_t *tags, int64_t n, int num_digits,
+                                     int64_t *bucket_offsets, int64_t *out_keys, uint64_t *out_tags,
+                                     cudaStream_t stream);
+hs_status_t hs_sort_chunks_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags,
+                                 int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
+                                 cudaStream_t stream);
+hs_status_t hs_merge_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags, int64_t n,
+                           hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
+                           cudaStream_t stream);
+
+/*
  * SURVEY §8(f) row f2, the sender side of the paper's cluster model with the
  * bucket exchange fused into the scatter (§3.4, "divides the data
  * into ten parts ... Then sends each bucket or buckets to proper node").

@@ -73,6 +73,10 @@ def _lib(openmp: bool = False):
         lib.oracle_msd_partition_pairs.restype = ci
         lib.oracle_sort_pairs.argtypes = [vp, vp, i64, ci, i64]
         lib.oracle_sort_pairs.restype = ci
+        lib.oracle_sort_chunks_pairs.argtypes = [vp, vp, i64, vp, i64]
+        lib.oracle_sort_chunks_pairs.restype = ci
+        lib.oracle_merge_pairs.argtypes = [vp, vp, i64, vp, i64]
+        lib.oracle_merge_pairs.restype = ci
         lib.oracle_sort_shared.argtypes = [vp, i64, i64]
         lib.oracle_sort_shared.restype = ci
         lib.oracle_openmp_threads.argtypes = []
@@ -209,6 +213,26 @@ def sort_pairs(keys, tags, num_digits: int, chunks: int = 8):
     k = _w(src)
     t = np.ascontiguousarray(np.asarray(tags).astype(np.uint64)).copy()
     _check(_lib().oracle_sort_pairs(_p(k), _p(t), k.size, num_digits, chunks))
+    return k.astype(src.dtype), t
+
+
+def sort_chunks_pairs(keys, tags, offsets, chunks: int):
+    """f3, a5 on items: each chunk sorted stably (Fig 1b merge sort).  Returns (keys, tags)."""
+    src = np.asarray(keys)
+    k = _w(src)
+    t = np.ascontiguousarray(np.asarray(tags).astype(np.uint64)).copy()
+    off = _w(offsets)
+    _check(_lib().oracle_sort_chunks_pairs(_p(k), _p(t), k.size, _p(off), chunks))
+    return k.astype(src.dtype), t
+
+
+def merge_pairs(keys, tags, offsets, chunks: int):
+    """f3, a6 on items: tree merge of each bucket's chunk runs, stable-left.  Returns (keys, tags)."""
+    src = np.asarray(keys)
+    k = _w(src)
+    t = np.ascontiguousarray(np.asarray(tags).astype(np.uint64)).copy()
+    off = _w(offsets)
+    _check(_lib().oracle_merge_pairs(_p(k), _p(t), k.size, _p(off), chunks))
     return k.astype(src.dtype), t
 
 

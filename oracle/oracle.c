@@ -396,6 +396,50 @@ int oracle_sort_pairs(int64_t *keys, uint64_t *tags, int64_t n, int num_digits, 
     return rc;
 }
 
+/* f3 phases as separate calls (the item forms of oracle_sort_chunks /
+ * oracle_merge): a5 -- every chunk (partition_even of each bucket of the
+ * given offsets) sorted by Fig 1b's non-recursive merge sort (stable);
+ * a6 -- the binary-tree merge of each bucket's chunk runs, round r merging
+ * runs [i, i+2^(r-1)) and [i+2^(r-1), i+2^r), stable-left.
+ * In place on keys / tags.                                                */
+int oracle_sort_chunks_pairs(int64_t *keys, uint64_t *tags, int64_t n, const int64_t *offsets11, int64_t c) {
+    if (!is_pow2(c)) return ORACLE_ERR_NOT_POW2;
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    int64_t *kb = (int64_t *)malloc(nn * sizeof(int64_t));
+    uint64_t *tb = (uint64_t *)malloc(nn * sizeof(uint64_t));
+    int64_t *lens = (int64_t *)malloc((size_t)c * sizeof(int64_t)), *starts = (int64_t *)malloc((size_t)(c + 1) * sizeof(int64_t));
+    int rc = (kb && tb && lens && starts) ? ORACLE_OK : ORACLE_ERR_NOMEM;
+    for (int b = 0; rc == ORACLE_OK && b < 10; b++) {
+        chunk_starts(offsets11[b], offsets11[b + 1] - offsets11[b], c, lens, starts);
+        for (int64_t i = 0; i < c; i++)
+            mergesort_items(keys + starts[i], tags + starts[i], lens[i], kb + starts[i], tb + starts[i]);
+    }
+    free(kb); free(tb); free(lens); free(starts);
+    return rc;
+}
+
+int oracle_merge_pairs(int64_t *keys, uint64_t *tags, int64_t n, const int64_t *offsets11, int64_t c) {
+    if (!is_pow2(c)) return ORACLE_ERR_NOT_POW2;
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    int64_t *kb = (int64_t *)malloc(nn * sizeof(int64_t));
+    uint64_t *tb = (uint64_t *)malloc(nn * sizeof(uint64_t));
+    int64_t *lens = (int64_t *)malloc((size_t)c * sizeof(int64_t)), *starts = (int64_t *)malloc((size_t)(c + 1) * sizeof(int64_t));
+    int rc = (kb && tb && lens && starts) ? ORACLE_OK : ORACLE_ERR_NOMEM;
+    for (int b = 0; rc == ORACLE_OK && b < 10; b++) {
+        chunk_starts(offsets11[b], offsets11[b + 1] - offsets11[b], c, lens, starts);
+        for (int64_t w = 1; w < c; w *= 2) {
+            for (int64_t i = 0; i < c; i += 2 * w) {
+                int64_t lo = starts[i], mid = starts[i + w], hi = starts[i + 2 * w];
+                merge_items(keys + lo, tags + lo, mid - lo, keys + mid, tags + mid, hi - mid, kb + lo, tb + lo);
+                memcpy(keys + lo, kb + lo, (size_t)(hi - lo) * sizeof(int64_t));
+                memcpy(tags + lo, tb + lo, (size_t)(hi - lo) * sizeof(uint64_t));
+            }
+        }
+    }
+    free(kb); free(tb); free(lens); free(starts);
+    return rc;
+}
+
 /* Reports whether this build runs the OpenMP pragmas (timing build). */
 int oracle_openmp_threads(void) {
 #ifdef _OPENMP

@@ -22,6 +22,7 @@ __all__ = [
     "hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared", "hs_sort_plan", "hs_sort_buckets", "hs_sort_host",
     "msd_partition", "sort_chunks", "merge", "sort", "sort_shared", "sort_host",
     "hs_msd_partition_pairs", "hs_sort_pairs", "msd_partition_pairs", "sort_pairs",
+    "hs_sort_chunks_pairs", "hs_merge_pairs", "sort_chunks_pairs", "merge_pairs",
     "abi_version", "tile_keys", "last_launch_count", "EXPORTED_SYMBOLS", "HostSortPipeline", "PartitionPlan", "SortGraph",
 ]
 
@@ -33,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "hs_profile_enable", "hs_profile_read", "hs_profile_kind_name", "hs_plan_levels", "hs_assign_buckets",
     "hs_msd_partition_pairs", "hs_sort_pairs",
     "hs_partition_plan_create", "hs_partition_scatter", "hs_partition_plan_destroy", "hs_sort_plan",
-    "hs_sort_buckets",
+    "hs_sort_buckets", "hs_sort_pairs64", "hs_msd_partition_pairs64", "hs_sort_chunks_pairs", "hs_merge_pairs",
 )
 PROFILE_KINDS = ("tile_hist", "tile_scan", "scatter", "plan", "tile_sort", "merge_partition", "merge_level", "copy",
                  "split_count", "split_scatter")
@@ -72,8 +73,13 @@ def load(path: str | None = None):
     lib.hs_sort_buckets.argtypes = [vp, i64, ci, ci, vp, ci, vp]
     lib.hs_msd_partition_pairs.argtypes = [vp, vp, i64, ci, vp, vp, vp, vp]
     lib.hs_sort_pairs.argtypes = [vp, vp, i64, ci, ci, vp]
+    lib.hs_sort_pairs64.argtypes = [vp, vp, i64, ci, ci, vp]
+    lib.hs_msd_partition_pairs64.argtypes = [vp, vp, i64, ci, vp, vp, vp, vp]
+    lib.hs_sort_chunks_pairs.argtypes = [vp, vp, vp, vp, i64, ci, vp, ci, vp]
+    lib.hs_merge_pairs.argtypes = [vp, vp, vp, vp, i64, ci, vp, ci, vp]
     for f in ("hs_msd_partition", "hs_sort_chunks", "hs_merge", "hs_sort", "hs_sort_shared",
-              "hs_msd_partition_pairs", "hs_sort_pairs", "hs_sort_plan", "hs_sort_buckets"):
+              "hs_msd_partition_pairs", "hs_sort_pairs", "hs_sort_plan", "hs_sort_buckets", "hs_sort_pairs64",
+              "hs_msd_partition_pairs64", "hs_sort_chunks_pairs", "hs_merge_pairs"):
         getattr(lib, f).restype = ci
     lib.hs_status_string.argtypes = [ci]
     lib.hs_status_string.restype = ctypes.c_char_p
@@ -319,37 +325,85 @@ def hs_sort_shared(keys, chunks: int = 8, stream=None):
     return keys
 
 
-def _check_pairs(keys, tags):
+def _check_pairs(keys, tags, int32_only: bool = False):
     torch = _torch()
     _check_tensor(keys, "keys")
     _check_tensor(tags, "tags")
-    if keys.dtype != torch.int32:
-        raise TypeError("hs_*_pairs: keys must be torch.int32")
-    if tags.element_size() != 8 or tags.numel() != keys.numel():
-        raise ValueError("tags must be a 64-bit tensor with one tag per key")
+    if int32_only and keys.dtype != torch.int32:
+        raise TypeError("keys must be torch.int32 here")
+    if keys.dtype not in (torch.int32, torch.int64):
+        raise TypeError(f"keys must be torch.int32 or torch.int64, got {keys.dtype}")
+    if tags.element_size() != 8 or tags.numel() != keys.numel() or tags.device != keys.device:
+        raise ValueError("tags must be a 64-bit tensor with one tag per key, on the keys' device")
 
 
 def hs_msd_partition_pairs(keys, tags, num_digits: int, stream=None):
-    """f3: stable MSD partition of (key, tag) items.  Returns (out_keys, out_tags, bucket_offsets)."""
+    """f3: stable MSD partition of (key, tag) items: within a bucket items keep
+    their input order.  int32 keys: (key << 32 | index) items; int64 keys: the KV item path
+    (hs_msd_partition_pairs64).  Returns (out_keys, out_tags, bucket_offsets)."""
     torch = _torch()
     _check_pairs(keys, tags)
     out_k = torch.empty_like(keys)
     out_t = torch.empty_like(tags)
     off = torch.empty(11, dtype=torch.int64, device=keys.device)
+    fn = load().hs_msd_partition_pairs if keys.dtype == torch.int32 else load().hs_msd_partition_pairs64
     with torch.cuda.device(keys.device):
-        _check(load().hs_msd_partition_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits,
-                                             off.data_ptr(), out_k.data_ptr(), out_t.data_ptr(), _stream(stream)))
+        _check(fn(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, off.data_ptr(), out_k.data_ptr(),
+                  out_t.data_ptr(), _stream(stream)))
     return out_k, out_t, off
 
 
 def hs_sort_pairs(keys, tags, num_digits: int, chunks_per_bucket: int = 8, stream=None):
-    """f3: stable sort of (key, tag) items in place (ties keep input order).  Returns (keys, tags)."""
+    """f3: stable sort of (key, tag) items in place (ties keep input order).  int32 keys go
+    through the keys path as (key << 32 | index) items (K5a split included) and the tags follow
+    their index; int64 keys through the stable KV item path (hs_sort_pairs64: tags travel with
+    their keys).  Returns (keys, tags)."""
     torch = _torch()
     _check_pairs(keys, tags)
+    fn = load().hs_sort_pairs if keys.dtype == torch.int32 else load().hs_sort_pairs64
     with torch.cuda.device(keys.device):
-        _check(load().hs_sort_pairs(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, chunks_per_bucket,
-                                    _stream(stream)))
+        _check(fn(keys.data_ptr(), tags.data_ptr(), keys.numel(), num_digits, chunks_per_bucket, _stream(stream)))
     return keys, tags
+
+
+def _pairs_outputs(keys, tags, bucket_offsets, out_keys, out_tags):
+    torch = _torch()
+    _check_pairs(keys, tags)
+    if out_keys is None:
+        out_keys = torch.empty_like(keys)
+    if out_tags is None:
+        out_tags = torch.empty_like(tags)
+    _check_pairs(out_keys, out_tags)
+    _check_out(keys, out_keys, bucket_offsets)
+    if out_tags.numel() != tags.numel() or out_tags.device != tags.device:
+        raise ValueError("out_tags must match tags in size and device")
+    return out_keys, out_tags
+
+
+def hs_sort_chunks_pairs(keys, tags, bucket_offsets, chunks_per_bucket: int = 8, out_keys=None, out_tags=None,
+                         stream=None):
+    """f3, a5 on items: every chunk of every bucket sorted stably (KV item path).  In place when
+    out_keys / out_tags are keys / tags.  Returns (out_keys, out_tags)."""
+    torch = _torch()
+    out_keys, out_tags = _pairs_outputs(keys, tags, bucket_offsets, out_keys, out_tags)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_sort_chunks_pairs(keys.data_ptr(), tags.data_ptr(), out_keys.data_ptr(), out_tags.data_ptr(),
+                                           keys.numel(), _dtype_code(keys), bucket_offsets.data_ptr(),
+                                           chunks_per_bucket, _stream(stream)))
+    return out_keys, out_tags
+
+
+def hs_merge_pairs(keys, tags, bucket_offsets, chunks_per_bucket: int = 8, out_keys=None, out_tags=None,
+                   stream=None):
+    """f3, a6 on items: the tree merge of each bucket's chunk-sorted runs of (key, tag) items with a
+    key-only comparator, ties taking the left run.  Returns (out_keys, out_tags)."""
+    torch = _torch()
+    out_keys, out_tags = _pairs_outputs(keys, tags, bucket_offsets, out_keys, out_tags)
+    with torch.cuda.device(keys.device):
+        _check(load().hs_merge_pairs(keys.data_ptr(), tags.data_ptr(), out_keys.data_ptr(), out_tags.data_ptr(),
+                                     keys.numel(), _dtype_code(keys), bucket_offsets.data_ptr(), chunks_per_bucket,
+                                     _stream(stream)))
+    return out_keys, out_tags
 
 
 class SortGraph:
@@ -511,4 +565,6 @@ sort = hs_sort
 sort_shared = hs_sort_shared
 sort_pairs = hs_sort_pairs
 msd_partition_pairs = hs_msd_partition_pairs
+sort_chunks_pairs = hs_sort_chunks_pairs
+merge_pairs = hs_merge_pairs
 sort_host = hs_sort_host

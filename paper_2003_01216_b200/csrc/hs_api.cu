@@ -67,6 +67,7 @@ cudaError_t device_setup(int *num_sms) {
         if (err == cudaSuccess) err = hs::setup_tilesort_kernels(dev);
         if (err == cudaSuccess) err = hs::setup_merge_kernels(dev);
         if (err == cudaSuccess) err = hs::setup_split_kernels(dev);
+        if (err == cudaSuccess) err = hs::setup_kv_kernels(dev);
     });
     if (err != cudaSuccess) return err;
     *num_sms = g_num_sms[dev];
@@ -878,3 +879,215 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, con
 }
 
 }  // extern "C"
+
+namespace {
+
+// f3 on KV64 items (k_kv.cu), in place on `items` (16-byte aligned scratch):
+//   kPlanSort:   a1-a3 (stable K3 on items) + a5 (stable tile sort + in-chunk levels) + a6 (tree levels)
+//   kPlanChunks: a5 only, chunks of the caller's bucket_offsets
+//   kPlanMerge:  a6 only, the caller's chunk-sorted runs
+// Every step is stable (k_kv.cu), so equal keys keep their input order.
+hs_status_t kv_impl(hs::KV64 *items, int64_t n, int num_digits, int log2c, int mode, const int64_t *user_off,
+                    int64_t *off_out, cudaStream_t stream) {
+    hs_status_t s;
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    constexpr int dt = 2;  // KV64
+    const int Tp = hs::scatter_tile_keys(dt), T = hs::kv_tile_keys(), TM = hs::merge_span(dt);
+    const long long ptiles = mode == hs::kPlanSort ? (n + Tp - 1) / Tp : 0;
+    const long long nblocks = (n + TM - 1) / TM;
+    unsigned long long div, magic;
+    digit_params(num_digits, HS_INT64, &div, &magic);
+    const int c = 1 << log2c;
+    Workspace ws;
+    if ((s = ws_alloc(&ws, (size_t)n * sizeof(hs::KV64), (size_t)hs::scan_ctas(ptiles) * 10, (size_t)ptiles,
+                      (size_t)nblocks + 2, (size_t)(n / hs::kSampleQ + 2) * sizeof(hs::KV64), stream)) != HS_OK)
+        return s;
+    const hs::Plan *plan = &ws.ctl->plan;
+    hs::KV64 *S = (hs::KV64 *)ws.S;
+    HS_TRY_CUDA(cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream), "memset control block");
+    int L = 0;
+    if (mode == hs::kPlanSort) {
+        // a1-a3: stable counting scatter of the items by the leading digit of their key, items -> S
+        HS_TRY_CUDA(hs::launch_partition(dt, items, S, (int)n, 0, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                         ws.status, (long long *)off_out, hs::kPlanSort, log2c, T, sms, true, stream),
+                    "K1-K3 partition (items)");
+        HS_TRY_CUDA(hs::launch_tile_sort_kv(plan, S, items, S, (hs::KV64 *)ws.samp[0], tile_bound(n, c, T), stream),
+                    "K5kv tile sort");
+        L = level_bound(n, log2c, T, 1, 1);
+    } else if (mode == hs::kPlanChunks) {
+        HS_TRY_CUDA(hs::launch_plan((const long long *)user_off, ws.ctl, log2c, hs::kPlanChunks, T, stream), "K4 plan");
+        HS_TRY_CUDA(hs::launch_tile_sort_kv(plan, items, items, S, (hs::KV64 *)ws.samp[0], tile_bound(n, c, T), stream),
+                    "K5kv tile sort");
+        L = level_bound(n, log2c, T, 1, 0);
+    } else {
+        HS_TRY_CUDA(hs::launch_plan((const long long *)user_off, ws.ctl, log2c, hs::kPlanMerge, 1, stream), "K4 plan");
+        HS_TRY_CUDA(hs::launch_sample(dt, items, ws.samp[0], n, sms, stream), "K6 sample");
+        // in place: level 0 reads the buffer its parity names (S when log2 c is odd)
+        if (log2c & 1) HS_TRY_CUDA(hs::launch_copy(dt, items, S, n, sms, stream), "K7 copy");
+        L = log2c;
+    }
+    for (int lv = 0; lv < L; ++lv) {
+        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, items, S, nullptr, ws.corank, ws.samp[lv & 1],
+                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
+                    "K6 merge level (items)");
+    }
+    cudaError_t fe = cudaFreeAsync(ws.base, stream);
+    if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    return HS_OK;
+}
+
+// Pack (keys, tags) into items, run kv_impl, unpack into (out_keys, out_tags).
+hs_status_t kv_call(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags, int64_t n,
+                    hs_dtype_t dtype, int num_digits, int log2c, int mode, const int64_t *user_off, int64_t *off_out,
+                    cudaStream_t stream) {
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    g_launch_counter = 0;
+    void *buf = nullptr;
+    const size_t ib = (size_t)n * sizeof(hs::KV64);
+    if ((e = cudaMallocAsync(&buf, ib, stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed", ib);
+    }
+    hs::KV64 *items = (hs::KV64 *)buf;
+    const int key64 = dtype == HS_INT64;
+    hs_status_t s = HS_OK;
+    if ((e = hs::launch_pack_kv(keys, key64, (const unsigned long long *)tags, items, n, sms, stream)) != cudaSuccess)
+        s = cuda_fail(e, "K0kv pack");
+    if (s == HS_OK) s = kv_impl(items, n, num_digits, log2c, mode, user_off, off_out, stream);
+    if (s == HS_OK &&
+        (e = hs::launch_unpack_kv(items, out_keys, key64, (unsigned long long *)out_tags, n, sms, stream)) != cudaSuccess)
+        s = cuda_fail(e, "K8kv unpack");
+    cudaError_t fe = cudaFreeAsync(buf, stream);
+    if (s != HS_OK) return s;
+    if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    return succeed();
+}
+
+hs_status_t check_kv_args(const void *keys, const uint64_t *tags, const void *out_keys, const uint64_t *out_tags,
+                          int64_t n, hs_dtype_t dtype, bool in_place_ok) {
+    hs_status_t s;
+    if ((s = check_common(n, dtype)) != HS_OK) return s;
+    if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
+    if ((s = check_ptr(out_keys, n, dtype, "out_keys")) != HS_OK) return s;
+    if ((s = check_ptr(tags, n, HS_INT64, "tags")) != HS_OK) return s;
+    if ((s = check_ptr(out_tags, n, HS_INT64, "out_tags")) != HS_OK) return s;
+    const size_t kb = (size_t)n * ksize(dtype), tb = (size_t)n * 8;
+    if (n > 0 && (overlap(keys, tags, kb > tb ? kb : tb) || overlap(out_keys, out_tags, kb > tb ? kb : tb)))
+        return fail(HS_ERR_INVALID_VALUE, "keys and tags overlap");
+    if (n > 0 && !in_place_ok && (overlap(keys, out_keys, kb) || overlap(tags, out_tags, tb)))
+        return fail(HS_ERR_INVALID_VALUE, "inputs and outputs overlap (out of place)");
+    if (n > 0 && in_place_ok && ((keys != out_keys && overlap(keys, out_keys, kb)) ||
+                                 (tags != out_tags && overlap(tags, out_tags, tb))))
+        return fail(HS_ERR_INVALID_VALUE, "inputs and outputs overlap without being equal");
+    return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hs_status_t hs_sort_pairs64(int64_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
+                            cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_kv_args(keys, tags, keys, tags, n, HS_INT64, true)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, HS_INT64)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    return kv_call(keys, tags, keys, tags, n, HS_INT64, num_digits, log2c, hs::kPlanSort, nullptr, nullptr, stream);
+}
+
+hs_status_t hs_msd_partition_pairs64(const int64_t *keys, const uint64_t *tags, int64_t n, int num_digits,
+                                     int64_t *bucket_offsets, int64_t *out_keys, uint64_t *out_tags,
+                                     cudaStream_t stream) {
+    hs_status_t s;
+    if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, HS_INT64, false)) != HS_OK) return s;
+    if ((s = check_digits(num_digits, HS_INT64)) != HS_OK) return s;
+    if (!bucket_offsets || ((uintptr_t)bucket_offsets & 7) != 0)
+        return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL or not 8-byte aligned");
+    if (n == 0) {  // offsets of an empty input: all zero
+        cudaError_t e = cudaMemsetAsync(bucket_offsets, 0, 11 * sizeof(int64_t), stream);
+        if (e != cudaSuccess) return cuda_fail(e, "memset bucket_offsets");
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    int sms;
+    cudaError_t e = device_setup(&sms);
+    if (e != cudaSuccess) return cuda_fail(e, "device setup");
+    g_launch_counter = 0;
+    void *buf = nullptr;
+    const size_t ib = (size_t)n * sizeof(hs::KV64);
+    if ((e = cudaMallocAsync(&buf, 2 * ib, stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HS_ERR_OUT_OF_MEMORY, "cudaMallocAsync(%zu bytes) failed", 2 * ib);
+    }
+    hs::KV64 *items = (hs::KV64 *)buf, *parted = items + n;
+    Workspace ws;
+    const int Tp = hs::scatter_tile_keys(2);
+    const long long tiles = (n + Tp - 1) / Tp;
+    unsigned long long div, magic;
+    digit_params(num_digits, HS_INT64, &div, &magic);
+    hs_status_t st = HS_OK;
+    if ((e = hs::launch_pack_kv(keys, 1, (const unsigned long long *)tags, items, n, sms, stream)) != cudaSuccess)
+        st = cuda_fail(e, "K0kv pack");
+    if (st == HS_OK) st = ws_alloc(&ws, 0, (size_t)hs::scan_ctas(tiles) * 10, (size_t)tiles, 0, 0, stream);
+    if (st == HS_OK) {
+        if ((e = cudaMemsetAsync(ws.ctl, 0, ws.zero_bytes, stream)) != cudaSuccess ||
+            (e = hs::launch_partition(2, items, parted, (int)n, 0, div, magic, ws.ctl, ws.tile_hist, ws.tile_pref,
+                                      ws.status, (long long *)bucket_offsets, -1, 0, 0, sms, true, stream)) !=
+                cudaSuccess ||
+            (e = hs::launch_unpack_kv(parted, out_keys, 1, (unsigned long long *)out_tags, n, sms, stream)) !=
+                cudaSuccess)
+            st = cuda_fail(e, "K1-K3 partition (items)");
+        cudaFreeAsync(ws.base, stream);
+    }
+    cudaError_t fe = cudaFreeAsync(buf, stream);
+    if (st != HS_OK) return st;
+    if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
+    return succeed();
+}
+
+hs_status_t hs_sort_chunks_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags,
+                                 int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
+                                 cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, dtype, true)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    return kv_call(keys, tags, out_keys, out_tags, n, dtype, 1, log2c, hs::kPlanChunks, bucket_offsets, nullptr,
+                   stream);
+}
+
+hs_status_t hs_merge_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags, int64_t n,
+                           hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
+                           cudaStream_t stream) {
+    hs_status_t s;
+    int log2c;
+    if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, dtype, true)) != HS_OK) return s;
+    if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
+    if (!bucket_offsets) return fail(HS_ERR_INVALID_VALUE, "bucket_offsets is NULL");
+    if (n == 0) {
+        g_launches = 0;
+        g_err[0] = 0;
+        return HS_OK;
+    }
+    return kv_call(keys, tags, out_keys, out_tags, n, dtype, 1, log2c, hs::kPlanMerge, bucket_offsets, nullptr, stream);
+}
+
+}  // extern "C"
+

@@ -47,6 +47,36 @@ struct KeyTraits<int64_t> {
     static constexpr int64_t kMax = 0x7fffffffffffffffLL;
 };
 
+// SURVEY f3 key + tag item of the stable path (hs_sort_pairs on int64 keys,
+// hs_merge_pairs, ...): SPEC's SortItem -- the tag travels with
+// its key through every pass and "never influences order": items compare by
+// key only, so equal keys keep whatever order the kernels give them, and the
+// kernels that see items are all stable (the K3 counting scatter, a stable
+// in-tile sort, stable-left merges).  16 bytes: one bulk-copy granule.
+struct __align__(16) KV64 {
+    long long k;
+    unsigned long long v;
+};
+__host__ __device__ __forceinline__ bool operator<(const KV64 &a, const KV64 &b) { return a.k < b.k; }
+__host__ __device__ __forceinline__ bool operator<=(const KV64 &a, const KV64 &b) { return a.k <= b.k; }
+__host__ __device__ __forceinline__ bool operator>(const KV64 &a, const KV64 &b) { return a.k > b.k; }
+template <>
+struct KeyTraits<KV64> {
+    using U = unsigned long long;
+    static constexpr KV64 kMax = {0x7fffffffffffffffLL, 0ull};
+};
+
+// Does a merge of K need explicit run ends?  Keys-only merges let an
+// exhausted run read as kMax (equal keys are interchangeable); items are not.
+template <typename K>
+struct ExactEnds {
+    static constexpr bool value = false;
+};
+template <>
+struct ExactEnds<KV64> {
+    static constexpr bool value = true;
+};
+
 // Leading decimal digit of a D-digit key, d(k) = clamp(floor(k / 10^(D-1)), 0, 9)
 // (reading #1 zero-padding, #3 clamping).  Division by the runtime
 // constant div = 10^(D-1) is exact by one multiply-high and a shift: magic =
@@ -70,6 +100,12 @@ __device__ __forceinline__ int msd_digit(int32_t k, const DigitParams<int32_t> &
 __device__ __forceinline__ int msd_digit(int64_t k, const DigitParams<int64_t> &p) {
     k >>= p.shift;  // arithmetic: keeps the sign of the key
     const unsigned long long u = (unsigned long long)(k > 0 ? k : 0);
+    const unsigned long long q = p.post >= 0 ? __umul64hi(u, p.magic) >> p.post : u;
+    return (int)(q < 9ull ? q : 9ull);
+}
+
+__device__ __forceinline__ int msd_digit(const KV64 &it, const DigitParams<KV64> &p) {
+    const unsigned long long u = (unsigned long long)(it.k > 0 ? it.k : 0);
     const unsigned long long q = p.post >= 0 ? __umul64hi(u, p.magic) >> p.post : u;
     return (int)(q < 9ull ? q : 9ull);
 }
@@ -449,6 +485,26 @@ __device__ __forceinline__ void st_keep(int64_t *p, int64_t v) {
         "st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p),
         "l"(v)
         : "memory");
+}
+
+__device__ __forceinline__ void st_keep(KV64 *p, KV64 v) {
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, pol;\n}" ::"l"(p),
+        "l"(v.k), "l"(v.v)
+        : "memory");
+}
+
+// Read-only cached load of a key (structs have no __ldg overload).
+template <typename K>
+__device__ __forceinline__ K ldg_key(const K *p) {
+    return __ldg(p);
+}
+template <>
+__device__ __forceinline__ KV64 ldg_key<KV64>(const KV64 *p) {
+    const longlong2 w = __ldg(reinterpret_cast<const longlong2 *>(p));
+    return KV64{w.x, (unsigned long long)w.y};
 }
 
 // Write the samples of output positions [x, x + len) whose keys sit at

@@ -1,6 +1,6 @@
 // hs_launch.h -- internal host-side launch interface between the C ABI
 // (hs_api.cu) and the kernels (k_partition.cu, k_tilesort.cu, k_merge.cu).
-// dt: 0 = int32, 1 = int64.
+// dt: 0 = int32, 1 = int64 (2 = KV64 items, internal: k_kv.cu).
 #pragma once
 
 #include <cstdint>
@@ -64,6 +64,18 @@ cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const
 // samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);
+
+// f3 key + tag items on the stable path (k_kv.cu).  dt 2 in the launchers
+// above (partition, merge level, sample, copy) = KV64 items.
+struct KV64;
+int kv_tile_keys();
+cudaError_t setup_kv_kernels(int dev);
+cudaError_t launch_pack_kv(const void *keys, int key64, const unsigned long long *tags, KV64 *items, long long n,
+                           int num_sms, cudaStream_t st);
+cudaError_t launch_unpack_kv(const KV64 *items, void *keys, int key64, unsigned long long *tags, long long n,
+                             int num_sms, cudaStream_t st);
+cudaError_t launch_tile_sort_kv(const Plan *plan, const KV64 *src, KV64 *F, KV64 *S, KV64 *samp, long long max_tiles,
+                                cudaStream_t st);
 
 // f3 key + tag items (k_pairs.cu)
 cudaError_t launch_pack_items(const int32_t *keys, long long *items, long long n, int num_sms, cudaStream_t st);

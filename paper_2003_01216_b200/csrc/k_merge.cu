@@ -52,6 +52,10 @@ template <>
 struct MGeo<int64_t> {
     static constexpr int kNT = HS_MERGE_NT, kVT = HS_MERGE_VT64, kST = HS_MERGE_ST;
 };
+template <>
+struct MGeo<KV64> {  // f3 items (k_kv.cu)
+    static constexpr int kNT = HS_MERGE_NT, kVT = 7, kST = HS_MERGE_ST;
+};
 
 template <typename K>
 __device__ __forceinline__ void bulk_s2g(K *dst, const K *src, uint32_t bytes) {
@@ -116,12 +120,12 @@ __global__ void k_merge_partition(const Plan *__restrict__ plan_g, K *F, K *S, c
             const long long pl = (g.b_lo + diag - 1 - mt) / Q * Q - 1;
             const long long pu = (g.b_lo + diag - 1 - mf) / Q * Q + Q - 1;
             if (tlo < thi) {
-                const bool t = pl >= g.b_lo && __ldg(samp + (g.a_lo + mt) / Q) <= __ldg(samp + pl / Q);
+                const bool t = pl >= g.b_lo && ldg_key(samp + (g.a_lo + mt) / Q) <= ldg_key(samp + pl / Q);
                 if (t) tlo = jt + 1;
                 else thi = jt;
             }
             if (flo < fhi) {
-                const bool f = pu < g.b_hi && __ldg(samp + (g.a_lo + mf) / Q) > __ldg(samp + pu / Q);
+                const bool f = pu < g.b_hi && ldg_key(samp + (g.a_lo + mf) / Q) > ldg_key(samp + pu / Q);
                 if (f) fhi = jf;
                 else flo = jf + 1;
             }
@@ -318,7 +322,8 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
             K y = bi < b_end ? sb[bi] : kMax;
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
-                const bool p = x <= y;
+                // items (ExactEnds): an exhausted run must never win a tie
+                const bool p = ExactEnds<K>::value ? (bi >= b_end || (ai < a_end && x <= y)) : x <= y;
                 v[k] = p ? x : y;
                 if (k + 1 < VT) {
                     const int nx = (p ? ai : bi) + 1;
@@ -416,7 +421,12 @@ int merge_span_t() {
     return MGeo<K>::kNT * MGeo<K>::kVT;
 }
 
-int g_merge_per_sm[kMaxDevices][2];  // resident K6b CTAs per SM, per device: [int32, int64]
+int g_merge_per_sm[kMaxDevices][3];  // resident K6b CTAs per SM, per device: [int32, int64, KV64]
+
+template <typename K>
+constexpr int kslot() {
+    return sizeof(K) == 4 ? 0 : sizeof(K) == 8 ? 1 : 2;
+}
 
 template <typename K>
 cudaError_t setup_merge_t(int dev) {
@@ -427,13 +437,14 @@ cudaError_t setup_merge_t(int dev) {
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::kNT + 32, SM::bytes());
-    g_merge_per_sm[dev][sizeof(K) == 8 ? 1 : 0] = occ > 0 ? occ : 1;
+    g_merge_per_sm[dev][kslot<K>()] = occ > 0 ? occ : 1;
     return e;
 }
 
 cudaError_t setup_merge_kernels(int dev) {
     cudaError_t e = setup_merge_t<int32_t>(dev);
-    return e != cudaSuccess ? e : setup_merge_t<int64_t>(dev);
+    if (e == cudaSuccess) e = setup_merge_t<int64_t>(dev);
+    return e != cudaSuccess ? e : setup_merge_t<KV64>(dev);
 }
 
 template <typename K>
@@ -447,7 +458,7 @@ cudaError_t launch_merge_level_t(const Plan *plan, void *F, void *S, const void 
     int dev = 0;
     cudaError_t e0 = cudaGetDevice(&dev);
     if (e0 != cudaSuccess) return e0;
-    const int per_sm = g_merge_per_sm[dev][sizeof(K) == 8 ? 1 : 0];
+    const int per_sm = g_merge_per_sm[dev][kslot<K>()];
     const int nblocks = (int)(((long long)n + TM - 1) / TM);
     if (nblocks == 0) return cudaSuccess;
     const int nbounds = nblocks + 1;
@@ -509,20 +520,26 @@ cudaError_t launch_copy_t(const void *src, void *dst, long long n, int num_sms, 
     return e;
 }
 
-int merge_span(int dt) { return dt == 0 ? merge_span_t<int32_t>() : merge_span_t<int64_t>(); }
+int merge_span(int dt) {
+    return dt == 0 ? merge_span_t<int32_t>() : dt == 1 ? merge_span_t<int64_t>() : merge_span_t<KV64>();
+}
 
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
                                const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st) {
+    if (dt == 2)
+        return launch_merge_level_t<KV64>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st);
     return dt == 0 ? launch_merge_level_t<int32_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st)
                    : launch_merge_level_t<int64_t>(plan, F, S, src0, corank, samp_in, samp_out, level, n, num_sms, st);
 }
 
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st) {
     (void)num_sms;
+    if (dt == 2) return launch_sample_t<KV64>(src, samp, n, st);
     return dt == 0 ? launch_sample_t<int32_t>(src, samp, n, st) : launch_sample_t<int64_t>(src, samp, n, st);
 }
 
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st) {
+    if (dt == 2) return launch_copy_t<KV64>(src, dst, n, num_sms, st);
     return dt == 0 ? launch_copy_t<int32_t>(src, dst, n, num_sms, st) : launch_copy_t<int64_t>(src, dst, n, num_sms, st);
 }
 

@@ -49,6 +49,10 @@ template <>
 struct PGeo<int64_t> {
     static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT / 2;
 };
+template <>
+struct PGeo<KV64> {  // f3 items (k_kv.cu): 16 bytes each
+    static constexpr int kScatNT = HS_SCAT_NT, kScatVT = HS_SCAT_VT / 4;
+};
 constexpr int kHistWarps = 8;
 constexpr int kScanNT = 256, kScanIPT = 8;  // 2048 tile histograms per K2 CTA
 
@@ -482,8 +486,8 @@ __global__ void __launch_bounds__(NT) k_scatter(const K *__restrict__ keys, K *_
 }
 
 // =============================================================== launchers
-// resident K3 CTAs per SM, per device: [int32, int64] x [local CSR, destination table]
-int g_scatter_per_sm[kMaxDevices][4];
+// resident K3 CTAs per SM, per device: [int32, int64] x [local CSR, destination table], KV64 items
+int g_scatter_per_sm[kMaxDevices][5];
 
 template <typename K, bool TABLE>
 cudaError_t setup_scatter_t(int dev, int slot) {
@@ -503,7 +507,8 @@ cudaError_t setup_partition_kernels(int dev) {
     if ((e = setup_scatter_t<int32_t, false>(dev, 0)) != cudaSuccess) return e;
     if ((e = setup_scatter_t<int64_t, false>(dev, 1)) != cudaSuccess) return e;
     if ((e = setup_scatter_t<int32_t, true>(dev, 2)) != cudaSuccess) return e;
-    return setup_scatter_t<int64_t, true>(dev, 3);
+    if ((e = setup_scatter_t<int64_t, true>(dev, 3)) != cudaSuccess) return e;
+    return setup_scatter_t<KV64, false>(dev, 4);
 }
 
 template <typename K>
@@ -551,11 +556,12 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     }
     if (e != cudaSuccess || !do_scatter || ntiles == 0) return e;
     using SS = ScatSmem<K, G::kScatNT, G::kScatVT>;
-    // local CSR output, or the destination-pointer table of hs_partition_scatter
-    auto kern = dst10 ? k_scatter<K, G::kScatNT, G::kScatVT, true> : k_scatter<K, G::kScatNT, G::kScatVT, false>;
+    // local CSR output, or the destination-pointer table of hs_partition_scatter (keys only)
+    auto kern = (dst10 && sizeof(K) <= 8) ? k_scatter<K, G::kScatNT, G::kScatVT, sizeof(K) <= 8>
+                                          : k_scatter<K, G::kScatNT, G::kScatVT, false>;
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    const int ki = (dst10 ? 2 : 0) + (sizeof(K) == 8 ? 1 : 0);
+    const int ki = sizeof(K) == 16 ? 4 : (dst10 ? 2 : 0) + (sizeof(K) == 8 ? 1 : 0);
     long long grid = (long long)g_scatter_per_sm[dev][ki] * num_sms;
     if (grid > ntiles) grid = ntiles;
     prof_begin(kProfScatter, st);
@@ -569,7 +575,9 @@ cudaError_t launch_partition_t(const void *keys, void *out, int n, int h, unsign
     return cudaGetLastError();
 }
 
-int scatter_tile_keys(int dt) { return dt == 0 ? scatter_tile_keys_t<int32_t>() : scatter_tile_keys_t<int64_t>(); }
+int scatter_tile_keys(int dt) {
+    return dt == 0 ? scatter_tile_keys_t<int32_t>() : dt == 1 ? scatter_tile_keys_t<int64_t>() : scatter_tile_keys_t<KV64>();
+}
 
 int scan_ctas(long long ntiles) {
     const long long per = (long long)kScanNT * kScanIPT;
@@ -581,6 +589,10 @@ cudaError_t launch_partition(int dt, const void *keys, void *out, int n, int h, 
                              unsigned long long *status, long long *user_off, int plan_mode, int log2c,
                              int sort_tile_keys, int num_sms, bool do_scatter, cudaStream_t st, int key_shift,
                              bool do_count, void *const *dst10) {
+    if (dt == 2)  // f3 items (k_kv.cu)
+        return launch_partition_t<KV64>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status, user_off,
+                                         plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, 0, st, do_count,
+                                         nullptr);
     return dt == 0 ? launch_partition_t<int32_t>(keys, out, n, h, div, magic, ctl, tile_hist, tile_pref, status,
                                                  user_off, plan_mode, log2c, sort_tile_keys, num_sms, do_scatter, 0, st,
                                                  do_count, dst10)
