@@ -83,6 +83,12 @@ bool overlap(const void *a, const void *b, size_t bytes) {
     return x < y + bytes && y < x + bytes;
 }
 
+// [a, a + na) and [b, b + nb) intersect
+bool overlap2(const void *a, size_t na, const void *b, size_t nb) {
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
 int ceil_log2(long long x) {
     int r = 0;
     while ((1LL << r) < x) ++r;
@@ -720,7 +726,8 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
     if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
     if ((s = check_ptr(keys, n, HS_INT32, "keys")) != HS_OK) return s;
     if ((s = check_ptr(tags, n, HS_INT64, "tags")) != HS_OK) return s;
-    if (n > 0 && overlap(keys, tags, (size_t)n * 4)) return fail(HS_ERR_INVALID_VALUE, "keys and tags overlap");
+    if (n > 0 && overlap2(keys, (size_t)n * 4, tags, (size_t)n * 8))
+        return fail(HS_ERR_INVALID_VALUE, "keys and tags overlap");
     if (n == 0) {
         g_launches = 0;
         g_err[0] = 0;
@@ -976,7 +983,8 @@ hs_status_t check_kv_args(const void *keys, const uint64_t *tags, const void *ou
     if ((s = check_ptr(tags, n, HS_INT64, "tags")) != HS_OK) return s;
     if ((s = check_ptr(out_tags, n, HS_INT64, "out_tags")) != HS_OK) return s;
     const size_t kb = (size_t)n * ksize(dtype), tb = (size_t)n * 8;
-    if (n > 0 && (overlap(keys, tags, kb > tb ? kb : tb) || overlap(out_keys, out_tags, kb > tb ? kb : tb)))
+    if (n > 0 && (overlap2(keys, kb, tags, tb) || overlap2(out_keys, kb, out_tags, tb) ||
+                  overlap2(keys, kb, out_tags, tb) || overlap2(out_keys, kb, tags, tb)))
         return fail(HS_ERR_INVALID_VALUE, "keys and tags overlap");
     if (n > 0 && !in_place_ok && (overlap(keys, out_keys, kb) || overlap(tags, out_tags, tb)))
         return fail(HS_ERR_INVALID_VALUE, "inputs and outputs overlap (out of place)");

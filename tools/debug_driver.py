@@ -25,6 +25,8 @@ def main():
     lib.hs_merge.argtypes = [vp, vp, i64, ci, vp, ci, vp]
     lib.hs_sort_shared.argtypes = [vp, i64, ci, ci, vp]
     lib.hs_sort_pairs.argtypes = [vp, vp, i64, ci, ci, vp]
+    lib.hs_sort_pairs64.argtypes = [vp, vp, i64, ci, ci, vp]
+    lib.hs_merge_pairs.argtypes = [vp, vp, vp, vp, i64, ci, vp, ci, vp]
     st = torch.cuda.current_stream().cuda_stream
     dev = "cuda:0"
     cases = 0
@@ -72,6 +74,23 @@ def main():
         rk, rt = O.sort_pairs(keys, tags.astype(np.uint64), 3, 8)
         assert np.array_equal(dk.cpu().numpy(), rk) and np.array_equal(dtg.cpu().numpy().view(np.uint64), rt)
         cases += 1
+        # f3 stable item path (k_kv.cu): int64 keys with ties, then a merge of chunk-sorted item runs
+        k64 = W.uniform(n, 5, 1000, dtype=np.int64) * 10**15
+        dk, dtg = torch.from_numpy(k64).to(dev), torch.from_numpy(tags).to(dev)
+        ok(lib.hs_sort_pairs64(dk.data_ptr(), dtg.data_ptr(), n, 18, 8, st))
+        torch.cuda.synchronize()
+        rk, rt = O.sort_pairs(k64, tags.astype(np.uint64), 18, 8)
+        assert np.array_equal(dk.cpu().numpy(), rk) and np.array_equal(dtg.cpu().numpy().view(np.uint64), rt)
+        pk, pt, poff = O.msd_partition_pairs(k64, tags.astype(np.uint64), 18)
+        ck, ct = O.sort_chunks_pairs(pk, pt, poff, 4)
+        dk, dtg, doff = (torch.from_numpy(ck).to(dev), torch.from_numpy(ct.view(np.int64)).to(dev),
+                         torch.from_numpy(poff).to(dev))
+        ok(lib.hs_merge_pairs(dk.data_ptr(), dtg.data_ptr(), dk.data_ptr(), dtg.data_ptr(), n, 1, doff.data_ptr(), 4,
+                              st))
+        torch.cuda.synchronize()
+        mk, mt = O.merge_pairs(ck, ct, poff, 4)
+        assert np.array_equal(dk.cpu().numpy(), mk) and np.array_equal(dtg.cpu().numpy().view(np.uint64), mt)
+        cases += 2
     # one full-size config through the debug checks
     keys = W.generate("C2")
     d = torch.from_numpy(keys).to(dev)
