@@ -1,6 +1,6 @@
 """Kernel-variant experiments (dev aid).
 
-  python tools/exp.py build NAME "-DHS_MERGE_VT=8 ..."   # -> exp/NAME/libhybridsort.so (here, no GPU)
+  python tools/exp.py build NAME "-DHS_MERGE_VT=8 ..."   # -> var/NAME/libhybridsort.so (here, no GPU)
   python tools/exp.py run NAME [NAME ...] [--cfg C3]    # on the GPU box: per-kernel device times
 
 Per-kernel times come from the CUPTI kernel trace of torch.profiler (device
@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 
 def build(name, defs):
     from paper_2003_01216_b200 import _build
-    out = os.path.join(ROOT, "exp", name)
+    out = os.path.join(ROOT, "var", name)
     os.makedirs(out, exist_ok=True)
     so = os.path.join(out, "libhybridsort.so")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, *defs.split(), "-I", _build.INCLUDE, "-I", _build.CSRC, "-o", so,
@@ -55,7 +55,7 @@ def run_merge1(name, cfg_name="C3", reps=5, chunks=2):
                 x[st0:st0 + ln] = torch.sort(x[st0:st0 + ln]).values
             st0 += ln
     torch.cuda.synchronize()
-    path = ROOT + "/paper_2003_01216_b200/libhybridsort.so" if name == "main" else os.path.join(ROOT, "exp", name, "libhybridsort.so")
+    path = ROOT + "/paper_2003_01216_b200/libhybridsort.so" if name == "main" else os.path.join(ROOT, "var", name, "libhybridsort.so")
     lib = hs.load(path)
     out = torch.empty_like(x)
     dt = 0 if x.dtype == torch.int32 else 1
@@ -88,7 +88,7 @@ def run(names, cfg_name="C3", reps=5):
     src = torch.from_numpy(W.generate(cfg_name)).cuda()
     buf = torch.empty_like(src)
     for name in names:
-        path = ROOT + "/paper_2003_01216_b200/libhybridsort.so" if name == "main" else os.path.join(ROOT, "exp", name, "libhybridsort.so")
+        path = ROOT + "/paper_2003_01216_b200/libhybridsort.so" if name == "main" else os.path.join(ROOT, "var", name, "libhybridsort.so")
         lib = hs.load(path)
         dt = 0 if src.dtype == torch.int32 else 1
         stream = torch.cuda.current_stream().cuda_stream
