@@ -189,6 +189,10 @@ struct SplitCfg {
 
 enum PlanMode { kPlanSort = 0, kPlanChunks = 1, kPlanMerge = 2 };
 
+// A K5a sub-range piece may hold up to 2^kBigLog2 tiles (duplicate-heavy or
+// skewed sub-ranges): its CTA sorts it as tiles + CTA-level merges (K5).
+constexpr int kBigLog2 = 2;
+
 __device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
     int r = 0;
     while ((1LL << r) < x) ++r;

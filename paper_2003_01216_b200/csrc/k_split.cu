@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
         uint32_t *row = tab + P.sboff[b] + j * (ns + 1);
         uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
         bool over = false;
-        for (int q = tid; q < ns; q += kSplitPlanNT) over |= row[q] > (uint32_t)tile_keys;
+        for (int q = tid; q < ns; q += kSplitPlanNT) over |= row[q] > ((uint32_t)tile_keys << kBigLog2);
         if (__syncthreads_or(over) && tid == 0) atomicOr(&C.bad, 1u << b);
         cta_excl_scan<kSplitPlanNT>(row, ns, wsum);
         for (int q = tid; q < ns; q += kSplitPlanNT) crow[q] = row[q];

@@ -112,6 +112,19 @@ __global__ void k_plan_whole(Ctl *ctl, long long n, int log2c, int tile_keys) {
 //      phase and leaves with one 1-D bulk async store (+ scalar head/tail).
 // This is the GPU shape of the paper's "sort partitions, then merge sorted
 // lists pairwise in a binary tree" at CTA scope.
+// Merge-path split of output diag between A[0..na) and B[0..nb) (stable-left: ties take A).
+template <typename K>
+__device__ __forceinline__ int merge_path_s(const K *A, int na, const K *B, int nb, int diag) {
+    int l = diag - nb > 0 ? diag - nb : 0;
+    int r = diag < na ? diag : na;
+    while (l < r) {
+        const int mid = (l + r) >> 1;
+        if (A[mid] <= B[diag - 1 - mid]) l = mid + 1;
+        else r = mid;
+    }
+    return l;
+}
+
 template <typename K>
 __device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
 template <typename K>
@@ -149,6 +162,46 @@ struct TSGeo {
     static constexpr int E = 16 / sizeof(K);
     static constexpr size_t bytes() { return (size_t)(T + 2 * E) * sizeof(K); }
 };
+
+// CTA-level streaming merge (the big-piece path of K5): O[0, na + nb) = stable-left
+// merge of A[0, na) and B[0, nb) (global memory; O disjoint from A and B), in
+// output windows of W = T / 3 keys: the next window's merge starts where this
+// one ended (no global search), its <= W keys of A and of B are loaded into
+// shared memory, every thread merges its outputs from a merge-path split with
+// explicit run ends, and the window leaves with coalesced stores (+ samples).
+template <typename K, int NT>
+__device__ void cta_merge(const K *A, int na, const K *B, int nb, K *O, K *sbuf, int T, K *samp, long long sx) {
+    const int W = T / 3, V = (W + NT - 1) / NT;
+    K *const sA = sbuf, *const sB = sbuf + W, *const sO = sbuf + 2 * W;
+    __shared__ int s_adv;
+    const int tid = threadIdx.x, n = na + nb;
+    int ai = 0, bi = 0;
+    for (int o = 0; o < n;) {
+        const int cnt = min(W, n - o);
+        const int la = min(cnt, na - ai), lb = min(cnt, nb - bi);
+        for (int j = tid; j < la; j += NT) sA[j] = A[ai + j];
+        for (int j = tid; j < lb; j += NT) sB[j] = B[bi + j];
+        __syncthreads();
+        const int p0 = min(tid * V, cnt), p1 = min(p0 + V, cnt);
+        if (p0 < p1) {
+            int a = merge_path_s(sA, la, sB, lb, p0), c = p0 - a;
+            for (int p = p0; p < p1; ++p) {
+                const bool tA = c >= lb || (a < la && sA[a] <= sB[c]);
+                sO[p] = tA ? sA[a] : sB[c];
+                a += tA ? 1 : 0;
+                c += tA ? 0 : 1;
+            }
+        }
+        if (tid == 0) s_adv = merge_path_s(sA, la, sB, lb, cnt);  // A keys consumed by this window
+        __syncthreads();
+        for (int j = tid; j < cnt; j += NT) O[o + j] = sO[j];
+        if (samp) write_samples(samp, sx + o, cnt, sO, tid, NT);
+        ai += s_adv;
+        bi += cnt - s_adv;
+        o += cnt;
+        __syncthreads();
+    }
+}
 
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
@@ -203,315 +256,355 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         len = (int)(leaf_start(P, b, i + 1) - lo);
     }
     if (len == 0) return;
-    HS_DASSERT(len > 0 && len <= T && lo >= P.off[b] && lo + len <= P.off[b + 1]);
-    K *const out = ((P.L[b] & 1) ? S : F) + lo;  // where this bucket's merge level 0 reads
+    HS_DASSERT(len > 0 && len <= ((long long)T << kBigLog2) && lo >= P.off[b] && lo + len <= P.off[b + 1]);
+    K *const fin_base = (P.L[b] & 1) ? S : F;  // where this bucket's merge level 0 reads
     const K kMax = KeyTraits<K>::kMax;
 
-    // 1. bulk load of the 16-byte aligned superset of the leaf
-    const K *in = src + lo;
-    const uintptr_t ga0 = (uintptr_t)in & ~(uintptr_t)15;
-    const uintptr_t ga1 = ((uintptr_t)(in + len) + 15) & ~(uintptr_t)15;
-    const int h = (int)(((uintptr_t)in - ga0) / sizeof(K));
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bar, (uint32_t)(ga1 - ga0));
-        bulk_g2s(sbuf, (const void *)ga0, (uint32_t)(ga1 - ga0), &bar);
-    }
-    K *const sm = sbuf + h;  // sm[0 .. len) = the leaf
-    mbar_wait(&bar, 0);
-    for (int j = len + tid; j < T; j += NT) sm[j] = kMax;
-    __syncthreads();
-
-    // 2. register sort of VT consecutive keys
-    K v[VT];
-    const bool live0 = tid * VT < len;
-#pragma unroll
-    for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
-    const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
-    K *const so = sbuf + sh;  // so[p] <-> out[p]
-    int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile / exact counting); 2: buckets to sort
-    // mode 2, int32: every bucket spans < 2^15 values, so a thread's two buckets are
-    // sorted together as 16-bit offsets packed two per register (see below)
-    bool packed = false;
-    constexpr int BPT_ = BUCKETS > 0 ? BUCKETS / NT : 1;
-    uint32_t bk_base = 0, bk_cnt[BPT_];  // mode 2: my buckets (set before mode becomes 2)
-
-    if constexpr (BUCKETS > 0) {
-        // 2'. Bucket pass (the usual case).  Keys are split by value into
-        // BUCKETS equal-width ranges of the tile's [min, max] (a monotone
-        // float scaling, so bucket order is key order), counted and scattered
-        // into so[] with shared-memory atomics, and every thread sorts its BPT
-        // buckets in registers (a CAP-key network).  About 3 shared accesses
-        // per key instead of ~2.6 per merge round; the merge rounds below
-        // remain the path for tiles with a bucket over CAP keys (skew, heavy
-        // duplicates) -- the result is the same unique sorted tile.  PACK:
-        // two 16-bit counters per word (int64 tiles: leaves room for 2 CTAs/SM).
-        constexpr int BPT = BUCKETS / NT;
-        constexpr bool PACK = sizeof(K) == 8 || BPT > 2;
-        static_assert(BUCKETS == BPT * NT && (!PACK || BPT % 2 == 0), "bucket layout");
-        __shared__ uint32_t bcnt[PACK ? BUCKETS / 2 : BUCKETS];
-        __shared__ K red[2][NT / 32];
-        __shared__ uint32_t wsum[NT / 32];
-        const int lane = tid & 31, warp = tid >> 5;
-        if (!frac) {
-            K lmin = kMax, lmax = (K)(-kMax - 1);
-#pragma unroll
-            for (int k = 0; k < VT; ++k)
-                if (tid * VT + k < len) {
-                    lmin = v[k] < lmin ? v[k] : lmin;
-                    lmax = v[k] > lmax ? v[k] : lmax;
-                }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                const K x = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
-                lmin = x < lmin ? x : lmin;
-                lmax = c > lmax ? c : lmax;
-            }
-            if (lane == 0) {
-                red[0][warp] = lmin;
-                red[1][warp] = lmax;
-            }
+    // Sort one tile: in[0, len) (len <= T) -> out[0, len).  phase: parity of the
+    // bulk-load barrier (one use per call); bulk: leave by one bulk async store
+    // (else plain stores: the big-piece path reads its own outputs back);
+    // samp_x >= 0: write the key samples of output positions samp_x + [0, len).
+    auto sort_tile = [&](const K *in, const int len, K *const out, const int phase, const bool bulk,
+                         const long long samp_x) {
+        // 1. bulk load of the 16-byte aligned superset of the leaf
+        const uintptr_t ga0 = (uintptr_t)in & ~(uintptr_t)15;
+        const uintptr_t ga1 = ((uintptr_t)(in + len) + 15) & ~(uintptr_t)15;
+        const int h = (int)(((uintptr_t)in - ga0) / sizeof(K));
+        if (tid == 0) {
+            mbar_arrive_expect_tx(&bar, (uint32_t)(ga1 - ga0));
+            bulk_g2s(sbuf, (const void *)ga0, (uint32_t)(ga1 - ga0), &bar);
         }
-#pragma unroll
-        for (int j = 0; j < (PACK ? BPT / 2 : BPT); ++j) bcnt[j * NT + tid] = 0;
-        __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
-        // bucket of k = mulhi(((k >> sft) - base) * mulA, M2): one integer map for all modes
-        //   frac:  base, mulA = the sub-range's (see above), M2 = BUCKETS (top bits of the fraction)
-        //   exact (range < BUCKETS): base = min, mulA = 2^w / BUCKETS, M2 = BUCKETS -> k - min
-        //   else:  base = min, mulA = 1, M2 = floor((2^w - 1) / (range + 1)) BUCKETS (< BUCKETS, monotone)
-        constexpr U WMAX = ~(U)0;
-        U base = f_base, mulA = f_mul, M2 = (U)BUCKETS;
-        int sft = f_sft;
-        bool exact = false, constant = false;
-        K mn = 0;
-        // frac: a bucket covers 2^w / (BUCKETS mul) + 1 values -- < 2^15 when mul >= 2^w / 2^24
-        packed = sizeof(K) == 4 && frac && f_mul >= (U)256;
-        if (!frac) {
-            mn = red[0][0];
-            K mx = red[1][0];
-#pragma unroll
-            for (int w = 1; w < NT / 32; ++w) {
-                mn = red[0][w] < mn ? red[0][w] : mn;
-                mx = red[1][w] > mx ? red[1][w] : mx;
-            }
-            const U range = (U)mx - (U)mn;
-            constant = range == 0;
-            exact = range < (U)BUCKETS;
-            base = (U)mn;
-            sft = 0;
-            if (exact) mulA = (U)(WMAX / (U)BUCKETS + 1);  // 2^w / BUCKETS
-            else {
-                mulA = 1;
-                M2 = range == WMAX ? (U)BUCKETS : WMAX / (range + 1) * (U)BUCKETS;
-            }
-            // a bucket spans about (range + 1) / BUCKETS values
-            packed = sizeof(K) == 4 && !exact && range < ((U)1 << 24);
-        }
-        if (constant) {  // constant tile: every order is the sorted one
-            for (int j = tid; j < len; j += NT) so[j] = mn;
-            mode = 1;
-        } else {
-            // exact: one bucket per key value (an exact counting sort, buckets need
-            // no sort and have no capacity limit)
-            auto bucket_of_key = [&](K k) -> int {
-                const U x = ((U)(k >> sft) - base) * mulA;
-                return (int)mulhi_u(x, M2);  // < BUCKETS, non-decreasing in k
-            };
-            // returns the bucket's count before this key (its slot when the counters hold starts)
-            auto bump = [&](int bk) -> uint32_t {
-                if (PACK) {
-                    const int sft = (bk & 1) * 16;
-                    return (atomicAdd(&bcnt[bk >> 1], 1u << sft) >> sft) & 0xFFFFu;
-                }
-                return atomicAdd(&bcnt[bk], 1u);
-            };
-            auto count_of = [&](int bk) -> uint32_t {
-                return PACK ? (bcnt[bk >> 1] >> ((bk & 1) * 16)) & 0xFFFFu : bcnt[bk];
-            };
-#pragma unroll
-            for (int k = 0; k < VT; ++k)
-                if (tid * VT + k < len) {
-                    const int bk = bucket_of_key(v[k]);
-                    if (PACK) atomicAdd(&bcnt[bk >> 1], 1u << ((bk & 1) * 16));  // no return: RED
-                    else atomicAdd(&bcnt[bk], 1u);
-                }
-            __syncthreads();
-            uint32_t cnt[BPT], tot = 0;
-            bool over = false;
-#pragma unroll
-            for (int q = 0; q < BPT; ++q) {
-                cnt[q] = count_of(BPT * tid + q);
-                tot += cnt[q];
-                over |= cnt[q] > (uint32_t)CAP;
-            }
-            if (!__syncthreads_or(!exact && over)) {
-                // exclusive scan of the per-thread totals -> bucket starts (cursors)
-                uint32_t incl = tot;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += u;
-                }
-                if (lane == 31) wsum[warp] = incl;
-                __syncthreads();
-                uint32_t base = incl - tot;
-                for (int w = 0; w < warp; ++w) base += wsum[w];
-                uint32_t st = base;
-                if (PACK) {
-#pragma unroll
-                    for (int q = 0; q < BPT; q += 2) {
-                        bcnt[(BPT * tid + q) >> 1] = st | ((st + cnt[q]) << 16);
-                        st += cnt[q] + cnt[q + 1];
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < BPT; ++q) {
-                        bcnt[BPT * tid + q] = st;
-                        st += cnt[q];
-                    }
-                }
-                __syncthreads();
-#pragma unroll
+        K *const sm = sbuf + h;  // sm[0 .. len) = the leaf
+        mbar_wait(&bar, phase & 1);
+        for (int j = len + tid; j < T; j += NT) sm[j] = kMax;
+        __syncthreads();
+
+        // 2. register sort of VT consecutive keys
+        K v[VT];
+        const bool live0 = tid * VT < len;
+    #pragma unroll
+        for (int k = 0; k < VT; ++k) v[k] = sm[tid * VT + k];
+        const int sh = (int)(((uintptr_t)out & 15) / sizeof(K));
+        K *const so = sbuf + sh;  // so[p] <-> out[p]
+        int mode = 0;  // 0: merge rounds; 1: tile staged (constant tile / exact counting); 2: buckets to sort
+        // mode 2, int32: every bucket spans < 2^15 values, so a thread's two buckets are
+        // sorted together as 16-bit offsets packed two per register (see below)
+        bool packed = false;
+        constexpr int BPT_ = BUCKETS > 0 ? BUCKETS / NT : 1;
+        uint32_t bk_base = 0, bk_cnt[BPT_];  // mode 2: my buckets (set before mode becomes 2)
+
+        if constexpr (BUCKETS > 0) {
+            // 2'. Bucket pass (the usual case).  Keys are split by value into
+            // BUCKETS equal-width ranges of the tile's [min, max] (a monotone
+            // float scaling, so bucket order is key order), counted and scattered
+            // into so[] with shared-memory atomics, and every thread sorts its BPT
+            // buckets in registers (a CAP-key network).  About 3 shared accesses
+            // per key instead of ~2.6 per merge round; the merge rounds below
+            // remain the path for tiles with a bucket over CAP keys (skew, heavy
+            // duplicates) -- the result is the same unique sorted tile.  PACK:
+            // two 16-bit counters per word (int64 tiles: leaves room for 2 CTAs/SM).
+            constexpr int BPT = BUCKETS / NT;
+            constexpr bool PACK = sizeof(K) == 8 || BPT > 2;
+            static_assert(BUCKETS == BPT * NT && (!PACK || BPT % 2 == 0), "bucket layout");
+            __shared__ uint32_t bcnt[PACK ? BUCKETS / 2 : BUCKETS];
+            __shared__ K red[2][NT / 32];
+            __shared__ uint32_t wsum[NT / 32];
+            const int lane = tid & 31, warp = tid >> 5;
+            if (!frac) {
+                K lmin = kMax, lmax = (K)(-kMax - 1);
+    #pragma unroll
                 for (int k = 0; k < VT; ++k)
-                    if (tid * VT + k < len) so[bump(bucket_of_key(v[k]))] = v[k];
-                bk_base = base;
-#pragma unroll
-                for (int q = 0; q < BPT; ++q) bk_cnt[q] = cnt[q];
-                mode = exact ? 1 : 2;
-            }
-        }
-    }
-
-    if (mode == 2 && packed) {
-        // int32, two buckets per thread, each spanning < 2^15 values: offsets from each
-        // bucket's first key (+2^15, so 0xFFFF pads sort last) packed two per register
-        // -- bucket 0 in the low halves, bucket 1 in the high halves -- and one CAP-key
-        // network of SIMD min/max sorts both buckets at once (half the comparators)
-        __syncthreads();
-        if constexpr (sizeof(K) == 4 && BPT_ == 2) {
-            const uint32_t stA = bk_base, cA = bk_cnt[0], stB = bk_base + bk_cnt[0], cB = bk_cnt[1];
-            if (cA > 1 || cB > 1) {
-                const int32_t rA = cA ? (int32_t)so[stA] : 0, rB = cB ? (int32_t)so[stB] : 0;
-                H2 w[CAP];
-#pragma unroll
-                for (int i = 0; i < CAP; ++i) {
-                    const uint32_t lo = i < (int)cA ? (uint32_t)((int32_t)so[stA + i] - rA + 32768) : 0xFFFFu;
-                    const uint32_t hi = i < (int)cB ? (uint32_t)((int32_t)so[stB + i] - rB + 32768) : 0xFFFFu;
-                    w[i].v = lo | (hi << 16);
+                    if (tid * VT + k < len) {
+                        lmin = v[k] < lmin ? v[k] : lmin;
+                        lmax = v[k] > lmax ? v[k] : lmax;
+                    }
+    #pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) {
+                    const K x = __shfl_xor_sync(0xffffffffu, lmin, o), c = __shfl_xor_sync(0xffffffffu, lmax, o);
+                    lmin = x < lmin ? x : lmin;
+                    lmax = c > lmax ? c : lmax;
                 }
-                oddeven_sort<CAP>(w);
-#pragma unroll
-                for (int i = 0; i < CAP; ++i) {
-                    if (i < (int)cA) so[stA + i] = (K)(rA + (int32_t)(w[i].v & 0xFFFFu) - 32768);
-                    if (i < (int)cB) so[stB + i] = (K)(rB + (int32_t)(w[i].v >> 16) - 32768);
+                if (lane == 0) {
+                    red[0][warp] = lmin;
+                    red[1][warp] = lmax;
                 }
             }
-        }
-    } else if (mode == 2) {
-        // sort my buckets in registers (v is dead on this path)
-        __syncthreads();
-        uint32_t st = bk_base;
-        constexpr int kBU = HS_SORT_BUNROLL;
-#pragma unroll kBU
-        for (int q = 0; q < BPT_; ++q) {
-            const uint32_t cn = bk_cnt[q];
-            if (cn > 1) {
-                K w[CAP];
-#pragma unroll
-                for (int i = 0; i < CAP; ++i) w[i] = i < (int)cn ? so[st + i] : kMax;
-                oddeven_sort<CAP>(w);
-#pragma unroll
-                for (int i = 0; i < CAP; ++i)
-                    if (i < (int)cn) so[st + i] = w[i];
+    #pragma unroll
+            for (int j = 0; j < (PACK ? BPT / 2 : BPT); ++j) bcnt[j * NT + tid] = 0;
+            __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
+            // bucket of k = mulhi(((k >> sft) - base) * mulA, M2): one integer map for all modes
+            //   frac:  base, mulA = the sub-range's (see above), M2 = BUCKETS (top bits of the fraction)
+            //   exact (range < BUCKETS): base = min, mulA = 2^w / BUCKETS, M2 = BUCKETS -> k - min
+            //   else:  base = min, mulA = 1, M2 = floor((2^w - 1) / (range + 1)) BUCKETS (< BUCKETS, monotone)
+            constexpr U WMAX = ~(U)0;
+            U base = f_base, mulA = f_mul, M2 = (U)BUCKETS;
+            int sft = f_sft;
+            bool exact = false, constant = false;
+            K mn = 0;
+            // frac: a bucket covers 2^w / (BUCKETS mul) + 1 values -- < 2^15 when mul >= 2^w / 2^24
+            packed = sizeof(K) == 4 && frac && f_mul >= (U)256;
+            if (!frac) {
+                mn = red[0][0];
+                K mx = red[1][0];
+    #pragma unroll
+                for (int w = 1; w < NT / 32; ++w) {
+                    mn = red[0][w] < mn ? red[0][w] : mn;
+                    mx = red[1][w] > mx ? red[1][w] : mx;
+                }
+                const U range = (U)mx - (U)mn;
+                constant = range == 0;
+                exact = range < (U)BUCKETS;
+                base = (U)mn;
+                sft = 0;
+                if (exact) mulA = (U)(WMAX / (U)BUCKETS + 1);  // 2^w / BUCKETS
+                else {
+                    mulA = 1;
+                    M2 = range == WMAX ? (U)BUCKETS : WMAX / (range + 1) * (U)BUCKETS;
+                }
+                // a bucket spans about (range + 1) / BUCKETS values
+                packed = sizeof(K) == 4 && !exact && range < ((U)1 << 24);
             }
-            st += cn;
+            if (constant) {  // constant tile: every order is the sorted one
+                for (int j = tid; j < len; j += NT) so[j] = mn;
+                mode = 1;
+            } else {
+                // exact: one bucket per key value (an exact counting sort, buckets need
+                // no sort and have no capacity limit)
+                auto bucket_of_key = [&](K k) -> int {
+                    const U x = ((U)(k >> sft) - base) * mulA;
+                    return (int)mulhi_u(x, M2);  // < BUCKETS, non-decreasing in k
+                };
+                // returns the bucket's count before this key (its slot when the counters hold starts)
+                auto bump = [&](int bk) -> uint32_t {
+                    if (PACK) {
+                        const int sft = (bk & 1) * 16;
+                        return (atomicAdd(&bcnt[bk >> 1], 1u << sft) >> sft) & 0xFFFFu;
+                    }
+                    return atomicAdd(&bcnt[bk], 1u);
+                };
+                auto count_of = [&](int bk) -> uint32_t {
+                    return PACK ? (bcnt[bk >> 1] >> ((bk & 1) * 16)) & 0xFFFFu : bcnt[bk];
+                };
+    #pragma unroll
+                for (int k = 0; k < VT; ++k)
+                    if (tid * VT + k < len) {
+                        const int bk = bucket_of_key(v[k]);
+                        if (PACK) atomicAdd(&bcnt[bk >> 1], 1u << ((bk & 1) * 16));  // no return: RED
+                        else atomicAdd(&bcnt[bk], 1u);
+                    }
+                __syncthreads();
+                uint32_t cnt[BPT], tot = 0;
+                bool over = false;
+    #pragma unroll
+                for (int q = 0; q < BPT; ++q) {
+                    cnt[q] = count_of(BPT * tid + q);
+                    tot += cnt[q];
+                    over |= cnt[q] > (uint32_t)CAP;
+                }
+                if (!__syncthreads_or(!exact && over)) {
+                    // exclusive scan of the per-thread totals -> bucket starts (cursors)
+                    uint32_t incl = tot;
+    #pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += u;
+                    }
+                    if (lane == 31) wsum[warp] = incl;
+                    __syncthreads();
+                    uint32_t base = incl - tot;
+                    for (int w = 0; w < warp; ++w) base += wsum[w];
+                    uint32_t st = base;
+                    if (PACK) {
+    #pragma unroll
+                        for (int q = 0; q < BPT; q += 2) {
+                            bcnt[(BPT * tid + q) >> 1] = st | ((st + cnt[q]) << 16);
+                            st += cnt[q] + cnt[q + 1];
+                        }
+                    } else {
+    #pragma unroll
+                        for (int q = 0; q < BPT; ++q) {
+                            bcnt[BPT * tid + q] = st;
+                            st += cnt[q];
+                        }
+                    }
+                    __syncthreads();
+    #pragma unroll
+                    for (int k = 0; k < VT; ++k)
+                        if (tid * VT + k < len) so[bump(bucket_of_key(v[k]))] = v[k];
+                    bk_base = base;
+    #pragma unroll
+                    for (int q = 0; q < BPT; ++q) bk_cnt[q] = cnt[q];
+                    mode = exact ? 1 : 2;
+                }
+            }
         }
-    } else if (mode == 0) {
-        if (live0) oddeven_sort<VT>(v);
 
-        // 3. merge rounds (R = threads per run).  Bitonic storage: in round R the
-        // input run q (length RL = R VT) is stored ascending if q is even (the
-        // pair's A) and DESCENDING if q is odd (the pair's B), so a pair occupies
-        // one bitonic stretch of shared memory.  A thread merges from both ends
-        // of what is left of it: the smaller of the two end keys is always the
-        // next output, even after one run is exhausted (the pointers then walk
-        // towards each other inside the other run), so the serial merge needs no
-        // bounds tests and no sentinels; ties take the A end (stable-left).
-        // Every thread stores every round (threads past the leaf's end hold
-        // kMax pads), so the stretch is complete; only threads with an output
-        // below len merge.
-        const uint32_t sm_u = smem_u32(sm);
-#pragma unroll 1
-        for (int lgR = 0; (1 << lgR) < NT; ++lgR) {
-            const int R = 1 << lgR, RL = R * VT;
-            const int q = tid >> lgR;  // this thread's outputs form part of input run q
-            __syncthreads();           // everyone has read the previous round's runs
-            if ((q & 1) == 0) {
-#pragma unroll
-                for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
-            } else {  // run q reversed in place: canonical c <-> (2q+1) RL - 1 - c
-                const int m = (2 * q + 1) * RL - 1 - tid * VT;
-#pragma unroll
-                for (int k = 0; k < VT; ++k) sm[m - k] = v[k];
+        if (mode == 2 && packed) {
+            // int32, two buckets per thread, each spanning < 2^15 values: offsets from each
+            // bucket's first key (+2^15, so 0xFFFF pads sort last) packed two per register
+            // -- bucket 0 in the low halves, bucket 1 in the high halves -- and one CAP-key
+            // network of SIMD min/max sorts both buckets at once (half the comparators)
+            __syncthreads();
+            if constexpr (sizeof(K) == 4 && BPT_ == 2) {
+                const uint32_t stA = bk_base, cA = bk_cnt[0], stB = bk_base + bk_cnt[0], cB = bk_cnt[1];
+                if (cA > 1 || cB > 1) {
+                    const int32_t rA = cA ? (int32_t)so[stA] : 0, rB = cB ? (int32_t)so[stB] : 0;
+                    H2 w[CAP];
+    #pragma unroll
+                    for (int i = 0; i < CAP; ++i) {
+                        const uint32_t lo = i < (int)cA ? (uint32_t)((int32_t)so[stA + i] - rA + 32768) : 0xFFFFu;
+                        const uint32_t hi = i < (int)cB ? (uint32_t)((int32_t)so[stB + i] - rB + 32768) : 0xFFFFu;
+                        w[i].v = lo | (hi << 16);
+                    }
+                    oddeven_sort<CAP>(w);
+    #pragma unroll
+                    for (int i = 0; i < CAP; ++i) {
+                        if (i < (int)cA) so[stA + i] = (K)(rA + (int32_t)(w[i].v & 0xFFFFu) - 32768);
+                        if (i < (int)cB) so[stB + i] = (K)(rB + (int32_t)(w[i].v >> 16) - 32768);
+                    }
+                }
             }
+        } else if (mode == 2) {
+            // sort my buckets in registers (v is dead on this path)
+            __syncthreads();
+            uint32_t st = bk_base;
+            constexpr int kBU = HS_SORT_BUNROLL;
+    #pragma unroll kBU
+            for (int q = 0; q < BPT_; ++q) {
+                const uint32_t cn = bk_cnt[q];
+                if (cn > 1) {
+                    K w[CAP];
+    #pragma unroll
+                    for (int i = 0; i < CAP; ++i) w[i] = i < (int)cn ? so[st + i] : kMax;
+                    oddeven_sort<CAP>(w);
+    #pragma unroll
+                    for (int i = 0; i < CAP; ++i)
+                        if (i < (int)cn) so[st + i] = w[i];
+                }
+                st += cn;
+            }
+        } else if (mode == 0) {
+            if (live0) oddeven_sort<VT>(v);
+
+            // 3. merge rounds (R = threads per run).  Bitonic storage: in round R the
+            // input run q (length RL = R VT) is stored ascending if q is even (the
+            // pair's A) and DESCENDING if q is odd (the pair's B), so a pair occupies
+            // one bitonic stretch of shared memory.  A thread merges from both ends
+            // of what is left of it: the smaller of the two end keys is always the
+            // next output, even after one run is exhausted (the pointers then walk
+            // towards each other inside the other run), so the serial merge needs no
+            // bounds tests and no sentinels; ties take the A end (stable-left).
+            // Every thread stores every round (threads past the leaf's end hold
+            // kMax pads), so the stretch is complete; only threads with an output
+            // below len merge.
+            const uint32_t sm_u = smem_u32(sm);
+    #pragma unroll 1
+            for (int lgR = 0; (1 << lgR) < NT; ++lgR) {
+                const int R = 1 << lgR, RL = R * VT;
+                const int q = tid >> lgR;  // this thread's outputs form part of input run q
+                __syncthreads();           // everyone has read the previous round's runs
+                if ((q & 1) == 0) {
+    #pragma unroll
+                    for (int k = 0; k < VT; ++k) sm[tid * VT + k] = v[k];
+                } else {  // run q reversed in place: canonical c <-> (2q+1) RL - 1 - c
+                    const int m = (2 * q + 1) * RL - 1 - tid * VT;
+    #pragma unroll
+                    for (int k = 0; k < VT; ++k) sm[m - k] = v[k];
+                }
+                __syncthreads();
+                if (tid * VT < len) {
+                    const int j = tid & (2 * R - 1);
+                    const int a0 = (tid - j) * VT, bE = a0 + 2 * RL;  // A = sm[a0, a0+RL) asc, B[k] = sm[bE-1-k]
+                    const int diag = j * VT;
+                    // merge path: first m with !(A[m] <= B[diag-1-m]); B[diag-1-m] = sm[bE - diag + m]
+                    int l = diag - RL > 0 ? diag - RL : 0, r = diag < RL ? diag : RL;
+                    const uint32_t ua = sm_u + (uint32_t)a0 * sizeof(K), ub = sm_u + (uint32_t)(bE - diag) * sizeof(K);
+                    while (l < r) {
+                        const int mid = (l + r) >> 1;
+                        const bool pr = lds_k<K>(ua + mid * (int)sizeof(K)) <= lds_k<K>(ub + mid * (int)sizeof(K));
+                        l = pr ? mid + 1 : l;
+                        r = pr ? r : mid;
+                    }
+                    uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
+                    uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
+                    HS_DASSERT(l >= 0 && l <= RL && diag - l >= 0 && diag - l <= RL && bE <= T);
+                    [[maybe_unused]] const uint32_t lo_b = ua, hi_b = sm_u + (uint32_t)bE * sizeof(K);  // the pair's stretch
+                    K x = lds_k<K>(pi), y = lds_k<K>(pj);
+    #pragma unroll
+                    for (int k = 0; k < VT; ++k) {
+                        const bool p = x <= y;
+                        v[k] = p ? x : y;
+                        if (k + 1 < VT) {
+                            pi += p ? (uint32_t)sizeof(K) : 0u;
+                            pj -= p ? 0u : (uint32_t)sizeof(K);
+                            HS_DASSERT(pi >= lo_b && pi < hi_b && pj >= lo_b && pj < hi_b);
+                            const K t = lds_k<K>(p ? pi : pj);
+                            x = p ? t : x;
+                            y = p ? y : t;
+                        }
+                    }
+                }
+            }
+
             __syncthreads();
             if (tid * VT < len) {
-                const int j = tid & (2 * R - 1);
-                const int a0 = (tid - j) * VT, bE = a0 + 2 * RL;  // A = sm[a0, a0+RL) asc, B[k] = sm[bE-1-k]
-                const int diag = j * VT;
-                // merge path: first m with !(A[m] <= B[diag-1-m]); B[diag-1-m] = sm[bE - diag + m]
-                int l = diag - RL > 0 ? diag - RL : 0, r = diag < RL ? diag : RL;
-                const uint32_t ua = sm_u + (uint32_t)a0 * sizeof(K), ub = sm_u + (uint32_t)(bE - diag) * sizeof(K);
-                while (l < r) {
-                    const int mid = (l + r) >> 1;
-                    const bool pr = lds_k<K>(ua + mid * (int)sizeof(K)) <= lds_k<K>(ub + mid * (int)sizeof(K));
-                    l = pr ? mid + 1 : l;
-                    r = pr ? r : mid;
-                }
-                uint32_t pi = ua + l * (int)sizeof(K);                                   // next A key
-                uint32_t pj = sm_u + (uint32_t)(bE - 1 - (diag - l)) * sizeof(K);       // next B key
-                HS_DASSERT(l >= 0 && l <= RL && diag - l >= 0 && diag - l <= RL && bE <= T);
-                [[maybe_unused]] const uint32_t lo_b = ua, hi_b = sm_u + (uint32_t)bE * sizeof(K);  // the pair's stretch
-                K x = lds_k<K>(pi), y = lds_k<K>(pj);
-#pragma unroll
-                for (int k = 0; k < VT; ++k) {
-                    const bool p = x <= y;
-                    v[k] = p ? x : y;
-                    if (k + 1 < VT) {
-                        pi += p ? (uint32_t)sizeof(K) : 0u;
-                        pj -= p ? 0u : (uint32_t)sizeof(K);
-                        HS_DASSERT(pi >= lo_b && pi < hi_b && pj >= lo_b && pj < hi_b);
-                        const K t = lds_k<K>(p ? pi : pj);
-                        x = p ? t : x;
-                        y = p ? y : t;
-                    }
-                }
+    #pragma unroll
+                for (int k = 0; k < VT; ++k) so[tid * VT + k] = v[k];
             }
-        }
+        }  // mode == 0
 
+        // 4. the sorted tile sits at the destination's 16-byte phase: bulk store the aligned middle
+        fence_proxy_async_smem();
         __syncthreads();
-        if (tid * VT < len) {
-#pragma unroll
-            for (int k = 0; k < VT; ++k) so[tid * VT + k] = v[k];
+        const int m0 = sh == 0 ? 0 : E - sh;            // first output at a 16-byte aligned address
+        const int m1 = (sh + len) / E * E - sh;         // end of the aligned middle
+        if (bulk && m1 > m0) {
+            if (tid == 0) {
+                bulk_s2g_ts(out + m0, so + m0, (uint32_t)((m1 - m0) * sizeof(K)));
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (tid < m0) out[tid] = so[tid];
+            else if (tid >= E && tid < 2 * E && m1 + tid - E < len) out[m1 + tid - E] = so[m1 + tid - E];
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        } else {
+            for (int p = tid; p < len; p += NT) out[p] = so[p];
         }
-    }  // mode == 0
+        if (samp_x >= 0) write_samples(samp, samp_x, len, so, tid, NT);  // coarse index for the next co-rank search
+    };
 
-    // 4. the sorted tile sits at the destination's 16-byte phase: bulk store the aligned middle
-    fence_proxy_async_smem();
-    __syncthreads();
-    const int m0 = sh == 0 ? 0 : E - sh;            // first output at a 16-byte aligned address
-    const int m1 = (sh + len) / E * E - sh;         // end of the aligned middle
-    if (m1 > m0) {
-        if (tid == 0) {
-            bulk_s2g_ts(out + m0, so + m0, (uint32_t)((m1 - m0) * sizeof(K)));
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (tid < m0) out[tid] = so[tid];
-        else if (tid >= E && tid < 2 * E && m1 + tid - E < len) out[m1 + tid - E] = so[m1 + tid - E];
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    } else {
-        for (int p = tid; p < len; p += NT) out[p] = so[p];
+    // A split piece longer than one tile (duplicate-heavy or skewed sub-ranges, up to
+    // 2^kBigLog2 tiles; k_split_plan sends longer ones to the bucket fallback): its
+    // 2^lgp parts (partition_even) are tile-sorted one after another, then lgp
+    // CTA-level merge passes (stable-left, P:58-60 at CTA scope) ping-pong between the
+    // piece's regions of F and S, the last one landing where merge level 0 reads.
+    int lgp = 0;
+    while (((long long)T << lgp) < len) ++lgp;
+    K *const fin = fin_base + lo;
+    if (lgp == 0) {
+        sort_tile(src + lo, len, fin, 0, true, lo);
+        return;
     }
-    write_samples(samp, lo, len, so, tid, NT);  // coarse index for merge level 0's co-rank search
+    K *const alt = (fin_base == F ? S : F) + lo;
+    K *xb = (lgp & 1) ? alt : fin;  // the parts' sorted runs; the last pass writes fin
+    for (int part = 0; part < (1 << lgp); ++part) {
+        const int ps = (int)part_start(len, lgp, part), pe = (int)part_start(len, lgp, part + 1);
+        __syncthreads();  // the previous part is done with shared memory
+        sort_tile(src + lo + ps, pe - ps, xb + ps, part, false, -1);
+    }
+    K *yb = xb == fin ? alt : fin;
+    for (int r = 0; r < lgp; ++r) {
+        const bool last = r + 1 == lgp;
+        for (int q = 0; q < (1 << (lgp - r - 1)); ++q) {  // runs = merged groups of 2^r parts
+            const int a0 = (int)part_start(len, lgp, (long long)(2 * q) << r);
+            const int a1 = (int)part_start(len, lgp, (long long)(2 * q + 1) << r);
+            const int a2 = (int)part_start(len, lgp, (long long)(2 * q + 2) << r);
+            __syncthreads();  // (the previous pass's / pair's outputs are written)
+            cta_merge<K, NT>(xb + a0, a1 - a0, xb + a1, a2 - a1, yb + a0, sbuf, T, last ? samp : nullptr, lo + a0);
+        }
+        K *const t = xb;
+        xb = yb;
+        yb = t;
+    }
 }
 
 // =============================================================== launchers

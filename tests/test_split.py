@@ -308,3 +308,21 @@ def test_split_density_ramp():
     rng.shuffle(keys)
     plan = check(keys, D, c)
     assert sum(plan["split"]) == 10, plan
+
+
+def test_split_big_pieces_sorted_in_cta():
+    """Sub-range pieces of 1-4 tiles (values with ~2.2 T copies per chunk, plus a narrow
+    non-constant peak): the bucket keeps the split -- such a piece is sorted by its CTA as tiles +
+    CTA-level merges (K5 big-piece path) instead of sending the bucket to the fallback."""
+    t, D, c = T(0), 9, 8
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(2024)
+    m = c * 3 * t
+    parts = [rng.integers(b * div, (b + 1) * div, size=m) for b in range(10)]
+    heavy = rng.integers(4 * div, 5 * div, size=5)
+    parts.append(np.repeat(heavy, int(2.2 * t) * c))                          # bucket 4: five heavy values
+    parts.append(rng.integers(7 * div + 1000, 7 * div + 1000 + 3 * t, size=int(2.5 * t) * c))  # bucket 7: dense
+    keys = np.concatenate(parts).astype(np.int32)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert plan["split"][4] == 1 and plan["split"][7] == 1, plan
