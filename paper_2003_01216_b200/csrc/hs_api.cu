@@ -170,7 +170,8 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     size_t k = round_up(corank_words * 4, 256);
     size_t sp = round_up(samp_bytes, 256);
     size_t sw = round_up(split_words * 4, 256);
-    size_t total = a + c + z + th + tp + k + 2 * sp + 2 * sw;
+    size_t swc = split_words ? round_up((size_t)hs::split_cur_words((long long)split_words) * 4, 256) : 0;
+    size_t total = a + c + z + th + tp + k + 2 * sp + sw + swc;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -486,7 +487,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                                       ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift);
         if (e2 == cudaSuccess && split_on)
             e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
-                                  stream);
+                                  F, stream);
         if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
         cudaError_t fe = cudaFreeAsync(ws.base, stream);
         if (e2 == cudaSuccess) e2 = fe;
@@ -510,13 +511,17 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                     "K1-K3 partition");
     }
     // a5 (K5a): value split of every chunk that exceeds one tile, part -> spl
+    // (constant pieces -- one key throughout, longer than the tile sort takes -- are filled straight
+    // into the tile sort's output buffer of split buckets: S for an odd number of chunk rounds)
+    void *const tile_out = (log2c & 1) ? ws.S : keys;
     if (split_on)
         HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, part, spl, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
-                                     key_shift, stream),
+                                     key_shift, tile_out, stream),
                     "K5a split");
     // a5: leaf-tile sort (part, or spl for split buckets) -> (keys | S) per bucket parity
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
-                                     ws.sbtab, &ws.ctl->split, spl),
+                                     ws.sbtab, &ws.ctl->split, spl,
+                                     split_on ? hs::split_cflag(ws.sbcur, split_words) : nullptr),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);

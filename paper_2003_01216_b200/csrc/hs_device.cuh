@@ -181,6 +181,7 @@ struct SplitCfg {
     int mode[10];                // 0: equal-width sub-ranges (mul); 1: sub-range = map[b][fine bin] (skewed bucket)
     int nsa[10];                 // split-table row capacity per chunk - 1 (nsb[b] <= nsa[b])
     int ns0[10];                 // equal-width sub-ranges per chunk (nsb[b] before any map)
+    int cc[10];                  // track constant sub-ranges (the sample saw a fine bin of > T keys per chunk)
     int map_chunks;              // sampled maps per bucket: c (one per chunk) or 1 (c > kMapChunksMax)
     unsigned bad;                // buckets with an over-full sub-range (fall back to merge levels)
     unsigned ticket;

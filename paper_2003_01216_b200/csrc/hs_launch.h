@@ -47,15 +47,21 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 struct SplitCfg;
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr,
-                             const SplitCfg *scfg = nullptr, const void *src_split = nullptr);  // null: F
+                             const SplitCfg *scfg = nullptr, const void *src_split = nullptr,  // null: F
+                             const uint32_t *cflag = nullptr);
 
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +
 // plan finalisation, scatter pass S -> F.  tab / cur hold tab_words words
 // (zeroed by k_split_setup before the count pass).
+// cur holds split_cur_words(tab_words) words (cursors + constant-piece tracking);
+// constant pieces (split_cflag) are written by the scatter straight to tile_out
+// (where the tile sort of split buckets writes) and skipped by the tile sort.
 long long split_table_words(long long n, int log2c, int tile_keys);
+long long split_cur_words(long long tab_words);
+const uint32_t *split_cflag(uint32_t *cur, long long tab_words);
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
-                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, void *tile_out,
                          cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
 // the samples this level writes for the next one (may be null).

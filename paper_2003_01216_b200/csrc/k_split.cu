@@ -92,8 +92,24 @@ __host__ __device__ __forceinline__ long long split_target(int tile_keys) {
 // keys (slack for the sampling error of the map).
 __host__ __device__ __forceinline__ long long split_target_map(int tile_keys) { return (long long)tile_keys * 7 / 10; }
 
+// Constant over-full sub-ranges (a value with more copies in a chunk than the
+// big-piece path takes, e.g. all keys equal): for buckets whose sample shows a
+// fine bin of more than a tile of keys per chunk (C.cc), the count pass also
+// records, per (chunk, sub-range), the min and max key (order-preserving
+// unsigned images; min kept as its complement so that both are atomicMax into
+// zeroed words).  A piece with min == max is already sorted: k_split_plan
+// flags it (cflag), the scatter writes it straight to where the tile sort's
+// output goes, and the tile sort only writes its key samples.
+struct SplitConst {
+    unsigned long long *gminc;  // ~u(min) per split-table word
+    unsigned long long *gmax;   // u(max)
+    uint32_t *cflag;            // 1: constant piece
+};
+__device__ __forceinline__ unsigned long long ukey(int32_t k) { return (unsigned long long)((uint32_t)k ^ 0x80000000u); }
+__device__ __forceinline__ unsigned long long ukey(int64_t k) { return (unsigned long long)k ^ 0x8000000000000000ull; }
+
 __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, int key_shift, int tile_keys,
-                              int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab) {
+                              int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab, SplitConst sc) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ long long s_words;
     if (threadIdx.x < 32) {  // lane b < 10: bucket b's geometry (64-bit divisions in parallel)
@@ -137,6 +153,7 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
             C.cand[b] = ok;
             C.mode[b] = 0;
             C.slice_prefix[b] = ac_s;
+            C.cc[b] = 0;
             if (ok) {
                 C.spc[b] = (int)spc;
                 P.nsb[b] = (int)ns;
@@ -164,7 +181,12 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
         }
     }
     __syncthreads();
-    for (long long q = threadIdx.x; q < s_words; q += blockDim.x) tab[q] = 0;
+    for (long long q = threadIdx.x; q < s_words; q += blockDim.x) {
+        tab[q] = 0;
+        sc.gminc[q] = 0;
+        sc.gmax[q] = 0;
+        sc.cflag[q] = 0;
+    }
 }
 
 // ------------------------------------------------------------------ sampled map
@@ -319,11 +341,25 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
         return total > 0 && ((float)s_max > mean_s + 5.0f * sqrtf(mean_s) + 1.0f ||
                              (float)cmax > mean_c + 5.0f * sqrtf(mean_c) + 1.0f);
     };
+    __shared__ unsigned s_binmax;
     for (int q = tid; q < kSplitFine; q += NT) h[q] = 0;
+    if (tid == 0) s_binmax = 0;
     __syncthreads();
     sample(false);
     __syncthreads();
     analyze();
+    {   // a fine bin holding more than a tile of keys per chunk: track constant sub-ranges in the count pass
+        uint32_t bm = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) bm = hv[j] > bm ? hv[j] : bm;
+        bm = __reduce_max_sync(0xffffffffu, bm);
+        if (lane == 0) atomicMax(&s_binmax, bm);
+        __syncthreads();
+        const long long cmk = (mb + (1LL << P.log2c) - 1) >> P.log2c;  // keys per chunk
+        if (tid == 0 && (unsigned long long)s_binmax * (unsigned long long)cmk >
+                            (unsigned long long)tile_keys * (unsigned long long)total)
+            C.cc[b] = 1;
+    }
     bool skewed = is_skewed();
     if (skewed) {  // uniform per CTA: the full sample for the map
         uint32_t h1[PER];
@@ -414,6 +450,7 @@ struct SliceDesc {
     unsigned long long mul, fmul;
     const uint16_t *bmap;    // sampled sub-range map of the bucket (null: equal width)
     int cnt, ns, shift, a0;  // keys in the slice (0: nothing to do), sub-ranges, item shift, offset in chunk
+    int cc;                  // track constant sub-ranges (SplitConst)
 };
 
 // Called by one thread (the fields share a few cache lines, so after the
@@ -443,6 +480,7 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
     sd.fmul = C.fmul[b];
     sd.bmap = C.mode[b] ? map + ((size_t)b * C.map_chunks + (C.map_chunks > 1 ? j : 0)) * kSplitFine : nullptr;
     sd.shift = C.shift;
+    sd.cc = C.cc[b];
 }
 
 // Count: persistent CTAs walk the slices with stride gridDim.x.  While the
@@ -451,14 +489,22 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
 // hist[ns] is a dummy sub-range for slots past a slice's end (branch-free).
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict__ ctl, const K *__restrict__ S,
-                                                          uint32_t *tab, int nsb_cap, const uint16_t *map) {
+                                                          uint32_t *tab, int nsb_cap, const uint16_t *map,
+                                                          SplitConst sc) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int TS = NT * VT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
+    // SplitConst tracking (slices of C.cc buckets): a key of each sub-range of the slice, and
+    // whether another key of the slice differs from it
+    K *const rep = reinterpret_cast<K *>(smem_raw + (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15));
+    unsigned char *const mixed = reinterpret_cast<unsigned char *>(rep + nsb_cap + 1);
     __shared__ SliceDesc sd[2];
     const int tid = threadIdx.x;
-    for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
+    for (int q = tid; q <= nsb_cap; q += NT) {
+        hist[q] = 0;
+        mixed[q] = 0;
+    }
     long long g = blockIdx.x;
     if (tid == 0) slice_desc(sd[0], ctl, g, false, TS, map);
     __syncthreads();
@@ -475,6 +521,13 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
         const SliceDesc &d = sd[cur];
         if (tid == 0) slice_desc(sd[cur ^ 1], ctl, g + gridDim.x, false, TS, map);
         const int cnt = d.cnt, ns = d.ns;
+        const bool cc = d.cc && cnt > 0;
+        // sub-range of slot k (slots past the slice's end: the dummy sub-range ns)
+        auto sub = [&](int k) -> int {
+            if (k * NT + tid >= cnt) return ns;
+            return d.bmap == nullptr ? sub_range_of(v[k], d.shift, d.lo, d.mul, ns)
+                                     : (int)__ldg(d.bmap + fine_bin<K>(v[k], d.shift, d.lo, d.fmul));
+        };
         if (cnt > 0) {
             HS_DASSERT(ns >= 2 && ns <= nsb_cap);
             if (d.bmap == nullptr) {  // equal width (uniform per slice: the branch is outside the key loop)
@@ -490,8 +543,20 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
                                                        : ns],
                               1u);
             }
+            if (cc) {
+#pragma unroll 4
+                for (int k = 0; k < VT; ++k) rep[sub(k)] = v[k];  // any one key of the sub-range wins
+            }
         }
         __syncthreads();  // histogram complete; next descriptor visible
+        if (cc) {
+#pragma unroll 4
+            for (int k = 0; k < VT; ++k) {
+                const int t = sub(k);
+                if (!(rep[t] <= v[k] && v[k] <= rep[t])) mixed[t] = 1;
+            }
+            __syncthreads();
+        }
         const SliceDesc &dn = sd[cur ^ 1];
         {
             const K *in = S + dn.cs + dn.a0;
@@ -502,8 +567,16 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
         if (cnt > 0) {
             for (int q = tid; q <= ns; q += NT) {
                 const uint32_t h = hist[q];
-                if (h && q < ns) atomicAdd(&tab[d.row + q], h);
+                if (h && q < ns) {
+                    atomicAdd(&tab[d.row + q], h);
+                    if (cc) {
+                        const unsigned long long u = mixed[q] ? ~0ull : ukey(rep[q]);
+                        atomicMax(&sc.gmax[d.row + q], u);
+                        atomicMax(&sc.gminc[d.row + q], mixed[q] ? ~0ull : ~u);  // mixed: min 0, max ~0
+                    }
+                }
                 hist[q] = 0;
+                mixed[q] = 0;
             }
         }
         __syncthreads();  // histogram zero again; sd[cur] may be overwritten
@@ -639,8 +712,43 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     }
 }
 
+// ------------------------------------------------------------- constant pieces
+// Every CTA walks the split tables of the buckets tracked for constant pieces
+// and writes, grid-strided inside each constant piece, its key over the piece's
+// range of tile_out (where the tile sort of split buckets writes); the tile
+// sort then only writes the piece's samples.  A fill, not a copy: the key is
+// the piece's min == max from the count pass.
+template <typename K>
+__global__ void __launch_bounds__(256) k_split_fill(const Ctl *__restrict__ ctl, const uint32_t *__restrict__ tab,
+                                                    SplitConst sc, K *tile_out) {
+    griddep_wait();  // PDL: the scatter has read its input (tile_out may be that buffer)
+    const Plan &P = ctl->plan;
+    const SplitCfg &C = ctl->split;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
+    for (int b = 0; b < 10; ++b) {
+        if (!P.split[b] || !C.cc[b]) continue;
+        const int ns = P.nsb[b], lg = P.log2c;
+        const long long m = P.off[b + 1] - P.off[b];
+        for (long long j = 0; j < (1LL << lg); ++j) {
+            const long long rb = P.sboff[b] + j * (ns + 1);
+            const long long cs = P.off[b] + part_start(m, lg, j);
+            for (int t = 0; t < ns; ++t) {
+                if (!sc.cflag[rb + t]) continue;
+                const unsigned long long u = sc.gmax[rb + t];
+                K val;
+                if constexpr (sizeof(K) == 4) val = (K)(int32_t)((uint32_t)u ^ 0x80000000u);
+                else val = (K)(long long)(u ^ 0x8000000000000000ull);
+                K *const o = tile_out + cs + tab[rb + t];
+                const long long len = (long long)tab[rb + t + 1] - tab[rb + t];
+                for (long long p = gtid; p < len; p += gstride) o[p] = val;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- per-chunk scan
-__global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t *tab, uint32_t *cur, int tile_keys) {
+__global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t *tab, uint32_t *cur, int tile_keys,
+                                                            SplitConst sc) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ uint32_t wsum[kSplitPlanNT / 32];
     __shared__ bool s_last;
@@ -655,7 +763,13 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
         uint32_t *row = tab + P.sboff[b] + j * (ns + 1);
         uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
         bool over = false;
-        for (int q = tid; q < ns; q += kSplitPlanNT) over |= row[q] > ((uint32_t)tile_keys << kBigLog2);
+        const long long rb = P.sboff[b] + j * (ns + 1);
+        for (int q = tid; q < ns; q += kSplitPlanNT) {
+            if (row[q] <= ((uint32_t)tile_keys << kBigLog2)) continue;  // the tile sort takes up to 2^kBigLog2 tiles
+            // longer: legal only if every key of the piece is the same (already sorted)
+            if (C.cc[b] && sc.gmax[rb + q] == ~sc.gminc[rb + q]) sc.cflag[rb + q] = 1;
+            else over = true;
+        }
         if (__syncthreads_or(over) && tid == 0) atomicOr(&C.bad, 1u << b);
         cta_excl_scan<kSplitPlanNT>(row, ns, wsum);
         for (int q = tid; q < ns; q += kSplitPlanNT) crow[q] = row[q];
@@ -700,6 +814,18 @@ static long long split_extra_words(int log2c) {  // the sampled maps (u16) after
     return 10LL * mc * kSplitFine / 2;
 }
 
+// The cursor region (split_cur_words) holds the cursors, then the SplitConst arrays.
+SplitConst split_const(uint32_t *cur, long long tab_words) {
+    const long long tw = (tab_words + 1) & ~1LL;  // 8-byte alignment of the 64-bit arrays
+    SplitConst sc;
+    sc.gminc = reinterpret_cast<unsigned long long *>(cur + tw);
+    sc.gmax = sc.gminc + tw;
+    sc.cflag = reinterpret_cast<uint32_t *>(sc.gmax + tw);
+    return sc;
+}
+
+long long split_cur_words(long long tab_words) { return 6 * ((tab_words + 1) & ~1LL); }
+
 long long split_table_words(long long n, int log2c, int tile_keys) {
     return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + split_extra_words(log2c);
 }
@@ -739,11 +865,12 @@ cudaError_t setup_split_kernels(int dev) {
 template <typename K>
 static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uint32_t *cur, long long tab_words,
                                   long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
-                                  cudaStream_t st) {
+                                  K *tile_out, cudaStream_t st) {
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
     const int nsb_cap = nsb_bound(n, log2c, tile_keys);
-    const size_t sm_count = (size_t)(nsb_cap + 1) * 4;
+    const size_t sm_count = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * (sizeof(K) + 1);
+    const SplitConst sc = split_const(cur, tab_words);
     const size_t sm_scat = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 +
                            (size_t)TS * (sizeof(K) + 4);
     auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT>;
@@ -758,7 +885,7 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     uint16_t *const map = reinterpret_cast<uint16_t *>(tab + tab_cap);
     prof_begin(kProfPlan, st);
     if ((e = launch_pdl(k_split_setup, dim3(1), dim3(1024), 0, st, ctl, div, 8 * (int)sizeof(K), key_shift,
-                        tile_keys, TS, tab_cap, nsb_cap, tab)) != cudaSuccess)
+                        tile_keys, TS, tab_cap, nsb_cap, tab, sc)) != cudaSuccess)
         return e;
     const int mc = (1LL << log2c) <= kMapChunksMax ? (int)(1LL << log2c) : 1;
     if ((e = launch_pdl(k_split_sample_map<K>, dim3(10 * mc), dim3(1024), 0, st, ctl, S, map, tile_keys)) !=
@@ -767,12 +894,13 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
-    if ((e = launch_pdl(kc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map)) != cudaSuccess)
+    if ((e = launch_pdl(kc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map, sc)) !=
+        cudaSuccess)
         return e;
     prof_end(kProfSplitCount, st);
     prof_begin(kProfPlan, st);
     if ((e = launch_pdl(k_split_plan, dim3((unsigned)(10 * c)), dim3(kSplitPlanNT), 0, st, ctl, tab, cur,
-                        tile_keys)) != cudaSuccess)
+                        tile_keys, sc)) != cudaSuccess)
         return e;
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
@@ -781,16 +909,23 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
         cudaSuccess)
         return e;
     prof_end(kProfSplitScatter, st);
+    prof_begin(kProfPlan, st);
+    if ((e = launch_pdl(k_split_fill<K>, dim3((unsigned)(2 * sms)), dim3(256), 0, st, (const Ctl *)ctl,
+                        (const uint32_t *)tab, sc, tile_out)) != cudaSuccess)
+        return e;
+    prof_end(kProfPlan, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
-                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
+                         long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, void *tile_out,
                          cudaStream_t st) {
     return dt == 0 ? launch_split_t<int32_t>(ctl, (const int32_t *)S, (int32_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, st)
+                                             tile_keys, div, key_shift, (int32_t *)tile_out, st)
                    : launch_split_t<int64_t>(ctl, (const int64_t *)S, (int64_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, st);
+                                             tile_keys, div, key_shift, (int64_t *)tile_out, st);
 }
+
+const uint32_t *split_cflag(uint32_t *cur, long long tab_words) { return split_const(cur, tab_words).cflag; }
 
 }  // namespace hs

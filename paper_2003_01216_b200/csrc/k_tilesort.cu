@@ -206,7 +206,8 @@ __device__ void cta_merge(const K *A, int na, const K *B, int nb, K *O, K *sbuf,
 template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp, const uint32_t *__restrict__ sbtab,
-                                                        const SplitCfg *__restrict__ scfg, const K *src_split) {
+                                                        const SplitCfg *__restrict__ scfg, const K *src_split,
+                                                        const uint32_t *__restrict__ cflag) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
@@ -244,6 +245,18 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
         len = (int)(__ldg(e + 1) - __ldg(e));
         src = src_split;
+        if (cflag && __ldg(cflag + (e - sbtab))) {
+            // a constant piece (k_split_plan): the scatter already wrote it where this kernel writes;
+            // only its key samples are left (every sample is that one key)
+            K *const o = ((P.L[b] & 1) ? S : F) + lo;
+            if (samp && len > 0) {
+                const K val = o[0];
+                const long long f = lo + (kSampleQ - 1 - lo % kSampleQ);
+                for (long long p = f + (long long)tid * kSampleQ; p < lo + len; p += (long long)NT * kSampleQ)
+                    st_keep(samp + p / kSampleQ, val);
+            }
+            return;
+        }
         const U mul = (U)scfg->mul[b];
         if (scfg->mode[b] == 0 && t > 0 && t < ns - 1 && mul <= (U)(~(U)0 >> 12)) {
             frac = true;
@@ -657,14 +670,15 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
-                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split) {
+                               cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split,
+                               const uint32_t *cflag) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)max_tiles), dim3(G::kNT), smem, st, plan, (const K *)src, (K *)F,
-                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F));
+                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F), cflag);
     if (e != cudaSuccess) return e;
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
@@ -672,9 +686,9 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg,
-                             const void *src_split) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split);
+                             const void *src_split, const uint32_t *cflag) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag);
 }
 
 }  // namespace hs

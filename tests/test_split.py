@@ -85,8 +85,11 @@ def test_split_just_over_one_tile():
 
 
 def test_split_mixed_with_fallback_buckets():
-    """Buckets 1, 4, 7 split (equal width), 6 splits through the sampled map (a narrow normal peak);
-    2 (one value), 5 (three values), 9 (clamped keys) fall back; 0, 3 fit a tile."""
+    """Buckets 1, 4, 7 split (equal width), 6 splits through the sampled map (a narrow normal peak),
+    9 (clamped keys pile into the last sub-range: 2.5 tiles per chunk) splits with a big piece (K5's
+    in-CTA tiles + merges), 2 (one value, 4.5 tiles per chunk) splits with a constant piece (filled,
+    not sorted); 5 (three values, 4.5 tiles per chunk in one sub-range: over the big-piece limit and
+    not constant) falls back; 0, 3 fit a tile."""
     t, D, c = T(0), 7, 2
     div = 10 ** (D - 1)
     rng = np.random.default_rng(3)
@@ -94,10 +97,10 @@ def test_split_mixed_with_fallback_buckets():
     parts = [
         rng.integers(0, div, size=t // 3),                     # bucket 0: small, no split needed
         rng.integers(div, 2 * div, size=m),                    # bucket 1: split
-        np.full(m, 2 * div + 12345),                           # bucket 2: constant -> over-full sub-range
+        np.full(9 * t, 2 * div + 12345),                       # bucket 2: constant -> sub-range over 4 tiles
         rng.integers(3 * div, 4 * div, size=t // 2),           # bucket 3: small
         rng.integers(4 * div, 5 * div, size=m + 999),          # bucket 4: split
-        5 * div + rng.integers(0, 3, size=m),                  # bucket 5: three values, > T copies each per chunk
+        5 * div + rng.integers(0, 3, size=9 * t),              # bucket 5: three values, 1.5 T copies each per chunk
         np.clip(rng.normal(6.5 * div, div / 40, size=m), 6 * div, 7 * div - 1).astype(np.int64),  # bucket 6: peak
         rng.integers(7 * div, 8 * div, size=m - 5),            # bucket 7: split
         rng.integers(10 * div, 2**31 - 1, size=m),             # bucket 9: clamped (>= 10^D): last sub-range
@@ -105,9 +108,9 @@ def test_split_mixed_with_fallback_buckets():
     keys = np.concatenate(parts).astype(np.int32)
     rng.shuffle(keys)
     plan = check(keys, D, c)
-    assert [plan["split"][b] for b in (1, 4, 6, 7)] == [1, 1, 1, 1]
-    assert [plan["split"][b] for b in (0, 2, 3, 5, 9)] == [0] * 5
-    assert plan["levels"][1] == 1 and plan["levels"][2] > 1    # fallback keeps its in-chunk levels
+    assert [plan["split"][b] for b in (1, 2, 4, 6, 7, 9)] == [1] * 6
+    assert [plan["split"][b] for b in (0, 3, 5)] == [0] * 3
+    assert plan["levels"][1] == 1 and plan["levels"][5] > 1    # fallback keeps its in-chunk levels
 
 
 def test_split_clamped_and_negative_inside_split_buckets():
@@ -326,3 +329,22 @@ def test_split_big_pieces_sorted_in_cta():
     rng.shuffle(keys)
     plan = check(keys, D, c)
     assert plan["split"][4] == 1 and plan["split"][7] == 1, plan
+
+
+@pytest.mark.parametrize("dtype,D", [(np.int32, 9), (np.int64, 18)])
+def test_split_constant_pieces(dtype, D):
+    """All keys of bucket 3 equal, and bucket 6 made of four values with ~6 tiles of copies per chunk
+    each (far apart: one value per sub-range): every over-full piece is constant, so both buckets keep
+    the split -- the pieces are filled from the count pass's min == max, not sorted."""
+    t, c = T(0 if dtype == np.int32 else 1), 8
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(606)
+    m = c * 3 * t
+    parts = [rng.integers(b * div, (b + 1) * div, size=m) for b in range(10) if b not in (3, 6)]
+    parts.append(np.full(c * 7 * t, 3 * div + 777))
+    vals = 6 * div + np.array([1, 3, 5, 7]) * (div // 9)
+    parts.append(np.repeat(vals, 6 * t * c))
+    keys = np.concatenate(parts).astype(dtype)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert plan["split"][3] == 1 and plan["split"][6] == 1, plan
