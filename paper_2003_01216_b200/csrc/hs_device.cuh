@@ -185,6 +185,7 @@ struct SplitCfg {
     int map_chunks;              // sampled maps per bucket: c (one per chunk) or 1 (c > kMapChunksMax)
     unsigned bad;                // buckets with an over-full sub-range (fall back to merge levels)
     unsigned ticket;
+    unsigned nconst;             // constant pieces listed for k_split_fill
     int shift;                   // sort key of an item = item >> shift (hs_sort_pairs)
 };
 

@@ -104,6 +104,7 @@ struct SplitConst {
     unsigned long long *gminc;  // ~u(min) per split-table word
     unsigned long long *gmax;   // u(max)
     uint32_t *cflag;            // 1: constant piece
+    unsigned long long *clist;  // constant pieces (split-table word, absolute chunk start), C.nconst of them
 };
 __device__ __forceinline__ unsigned long long ukey(int32_t k) { return (unsigned long long)((uint32_t)k ^ 0x80000000u); }
 __device__ __forceinline__ unsigned long long ukey(int64_t k) { return (unsigned long long)k ^ 0x8000000000000000ull; }
@@ -355,9 +356,12 @@ __global__ void __launch_bounds__(1024) k_split_sample_map(Ctl *ctl, const K *__
         bm = __reduce_max_sync(0xffffffffu, bm);
         if (lane == 0) atomicMax(&s_binmax, bm);
         __syncthreads();
+        // a piece over the big-piece limit (2^kBigLog2 tiles) needs a bin of many copies; ask for
+        // two tiles' worth of a chunk and >= 32 samples (far above the noise of a smooth density)
         const long long cmk = (mb + (1LL << P.log2c) - 1) >> P.log2c;  // keys per chunk
-        if (tid == 0 && (unsigned long long)s_binmax * (unsigned long long)cmk >
-                            (unsigned long long)tile_keys * (unsigned long long)total)
+        if (tid == 0 && s_binmax >= 32 &&
+            (unsigned long long)s_binmax * (unsigned long long)cmk >
+                2ull * (unsigned long long)tile_keys * (unsigned long long)total)
             C.cc[b] = 1;
     }
     bool skewed = is_skewed();
@@ -487,11 +491,18 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
 // shared histogram of slice g is flushed to its chunk's row (and re-zeroed by
 // the same threads), the keys of the CTA's next slice are already loading.
 // hist[ns] is a dummy sub-range for slots past a slice's end (branch-free).
-template <typename K, int NT, int VT, int MINB>
+// CC = false: slices of buckets without constant tracking (the usual case, no extra work);
+// CC = true: only slices of C.cc buckets, with the tracking (exits at once when there are none).
+template <typename K, int NT, int VT, int MINB, bool CC>
 __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                           uint32_t *tab, int nsb_cap, const uint16_t *map,
                                                           SplitConst sc) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
+    if (CC) {
+        bool any = false;
+        for (int b = 0; b < 10; ++b) any |= ctl->split.cc[b] != 0;
+        if (!any) return;
+    }
     constexpr int TS = NT * VT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
@@ -512,7 +523,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
     K v[VT];
     {
         const K *in = S + sd[0].cs + sd[0].a0;
-        const int cnt = sd[0].cnt;
+        const int cnt = (sd[0].cc != 0) == CC ? sd[0].cnt : 0;
 #pragma unroll
         for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
     }
@@ -520,8 +531,8 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
     for (; g < nslices; g += gridDim.x) {
         const SliceDesc &d = sd[cur];
         if (tid == 0) slice_desc(sd[cur ^ 1], ctl, g + gridDim.x, false, TS, map);
-        const int cnt = d.cnt, ns = d.ns;
-        const bool cc = d.cc && cnt > 0;
+        const int cnt = (d.cc != 0) == CC ? d.cnt : 0, ns = d.ns;  // this instantiation's slices only
+        constexpr bool cc = CC;
         // sub-range of slot k (slots past the slice's end: the dummy sub-range ns)
         auto sub = [&](int k) -> int {
             if (k * NT + tid >= cnt) return ns;
@@ -560,7 +571,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
         const SliceDesc &dn = sd[cur ^ 1];
         {
             const K *in = S + dn.cs + dn.a0;
-            const int cn = dn.cnt;
+            const int cn = (dn.cc != 0) == CC ? dn.cnt : 0;
 #pragma unroll
             for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cn ? in[k * NT + tid] : K(0);
         }
@@ -722,27 +733,17 @@ template <typename K>
 __global__ void __launch_bounds__(256) k_split_fill(const Ctl *__restrict__ ctl, const uint32_t *__restrict__ tab,
                                                     SplitConst sc, K *tile_out) {
     griddep_wait();  // PDL: the scatter has read its input (tile_out may be that buffer)
-    const Plan &P = ctl->plan;
-    const SplitCfg &C = ctl->split;
+    const unsigned nc = ctl->split.nconst;
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
-    for (int b = 0; b < 10; ++b) {
-        if (!P.split[b] || !C.cc[b]) continue;
-        const int ns = P.nsb[b], lg = P.log2c;
-        const long long m = P.off[b + 1] - P.off[b];
-        for (long long j = 0; j < (1LL << lg); ++j) {
-            const long long rb = P.sboff[b] + j * (ns + 1);
-            const long long cs = P.off[b] + part_start(m, lg, j);
-            for (int t = 0; t < ns; ++t) {
-                if (!sc.cflag[rb + t]) continue;
-                const unsigned long long u = sc.gmax[rb + t];
-                K val;
-                if constexpr (sizeof(K) == 4) val = (K)(int32_t)((uint32_t)u ^ 0x80000000u);
-                else val = (K)(long long)(u ^ 0x8000000000000000ull);
-                K *const o = tile_out + cs + tab[rb + t];
-                const long long len = (long long)tab[rb + t + 1] - tab[rb + t];
-                for (long long p = gtid; p < len; p += gstride) o[p] = val;
-            }
-        }
+    for (unsigned i = 0; i < nc; ++i) {
+        const long long w = (long long)sc.clist[2 * i], cs = (long long)sc.clist[2 * i + 1];
+        const unsigned long long u = sc.gmax[w];
+        K val;
+        if constexpr (sizeof(K) == 4) val = (K)(int32_t)((uint32_t)u ^ 0x80000000u);
+        else val = (K)(long long)(u ^ 0x8000000000000000ull);
+        K *const o = tile_out + cs + tab[w];
+        const long long len = (long long)tab[w + 1] - tab[w];
+        for (long long p = gtid; p < len; p += gstride) o[p] = val;
     }
 }
 
@@ -767,8 +768,14 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
         for (int q = tid; q < ns; q += kSplitPlanNT) {
             if (row[q] <= ((uint32_t)tile_keys << kBigLog2)) continue;  // the tile sort takes up to 2^kBigLog2 tiles
             // longer: legal only if every key of the piece is the same (already sorted)
-            if (C.cc[b] && sc.gmax[rb + q] == ~sc.gminc[rb + q]) sc.cflag[rb + q] = 1;
-            else over = true;
+            if (C.cc[b] && sc.gmax[rb + q] == ~sc.gminc[rb + q]) {
+                sc.cflag[rb + q] = 1;
+                const unsigned slot = atomicAdd(&C.nconst, 1u);  // k_split_fill's work list
+                sc.clist[2 * slot] = (unsigned long long)(rb + q);
+                sc.clist[2 * slot + 1] = (unsigned long long)(P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j));
+            } else {
+                over = true;
+            }
         }
         if (__syncthreads_or(over) && tid == 0) atomicOr(&C.bad, 1u << b);
         cta_excl_scan<kSplitPlanNT>(row, ns, wsum);
@@ -821,10 +828,11 @@ SplitConst split_const(uint32_t *cur, long long tab_words) {
     sc.gminc = reinterpret_cast<unsigned long long *>(cur + tw);
     sc.gmax = sc.gminc + tw;
     sc.cflag = reinterpret_cast<uint32_t *>(sc.gmax + tw);
+    sc.clist = reinterpret_cast<unsigned long long *>(sc.cflag + tw);
     return sc;
 }
 
-long long split_cur_words(long long tab_words) { return 6 * ((tab_words + 1) & ~1LL); }
+long long split_cur_words(long long tab_words) { return 10 * ((tab_words + 1) & ~1LL); }
 
 long long split_table_words(long long n, int log2c, int tile_keys) {
     return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + split_extra_words(log2c);
@@ -843,11 +851,14 @@ template <typename K>
 cudaError_t setup_split_t() {
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
-    const size_t sm_count = (size_t)(kSplitMaxSub + 1) * 4;
+    const size_t sm_count = (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * (sizeof(K) + 1);
     const size_t sm_scat = (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * 8 +
                            (size_t)TS * (sizeof(K) + 4);
-    cudaError_t e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT>,
+    cudaError_t e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat);
@@ -873,7 +884,8 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     const SplitConst sc = split_const(cur, tab_words);
     const size_t sm_scat = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 +
                            (size_t)TS * (sizeof(K) + 4);
-    auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT>;
+    auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, false>;
+    auto kcc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, true>;
     auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>;
     cudaError_t e;
     int dev = 0;
@@ -895,6 +907,9 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
     if ((e = launch_pdl(kc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map, sc)) !=
+        cudaSuccess)
+        return e;
+    if ((e = launch_pdl(kcc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map, sc)) !=
         cudaSuccess)
         return e;
     prof_end(kProfSplitCount, st);

@@ -38,5 +38,12 @@ for name, make in cases.items():
     ok = bool((b[1:] >= b[:-1]).all()) and b.long().sum().item() == s1 and abs((b.double() ** 2).sum().item() - s2) <= 1e-9 * s2
     ms = sorted(ts)[1]
     print(f"{name:28s} {ms:7.3f} ms {n / ms / 1e6:6.1f} Gkeys/s  ok={ok}  split={plan['split']}  levels={plan['levels']}")
+    if "--kernels" in sys.argv:
+        b = k.clone()
+        hs.profile_enable(True)
+        hs.hs_sort(b, 9, 8)
+        prof = hs.profile_read()
+        hs.profile_enable(False)
+        print("      " + "  ".join(f"{kk} {v[0]:.3f}" for kk, v in sorted(prof.items(), key=lambda kv: -kv[1][0]) if v[1]))
     del k, b
     torch.cuda.empty_cache()
