@@ -236,9 +236,7 @@ def run_ours(args, cfg):
 
     shared = args.api == "shared"
     pairs = args.api == "pairs"
-    if pairs:
-        if cfg.dtype != "int32":
-            raise SystemExit("--api pairs needs an int32 config (f3 items are int32 keys + 64-bit tags)")
+    if pairs:  # f3: int32 keys -> (key << 32 | index) items + tag gather; int64 keys -> the stable KV item path
         tags0 = torch.arange(cfg.n, dtype=torch.int64, device=dev)
         tags = torch.empty_like(tags0)
 
@@ -322,13 +320,20 @@ def run_ours(args, cfg):
     else:
         _, off = hs.hs_msd_partition(src, cfg.num_digits)
         off_h = off.cpu().numpy()
+    kv = pairs and cfg.dtype == "int64"
     levels, tile_levels = hs.plan_levels(off_h, 1 if pairs else dt_code, cfg.chunks, 0)
+    if kv:  # the item path's own tile capacity (no K5a split on it)
+        t_kv, c = hs.tile_keys(1, 3), cfg.chunks
+        levels = []
+        for mm in np.diff(off_h).tolist():
+            tiles = -(-(-(-mm // c)) // t_kv)  # ceil(ceil(m / c) / T)
+            levels.append((int(tiles - 1).bit_length() if tiles > 1 else 0) + c.bit_length() - 1)
     split = [0] * 10
     if not shared and not pairs:  # the device plan: which buckets the K5a value split took
         dplan = hs.hs_sort_plan(src, cfg.num_digits, cfg.chunks)
         levels, split = dplan["levels"], dplan["split"]
     if pairs:
-        ksize = 8  # the items (key << 32 | index) travel through the int64 path
+        ksize = 16 if kv else 8  # KV64 items, or (key << 32 | index) items through the int64 path
     m = np.diff(off_h)
     per_kernel = {}
     for kind, (tot, cnt) in prof.items():
@@ -360,8 +365,10 @@ def run_ours(args, cfg):
                 "active_launches_per_step": len(active) if dom == "merge_level" else 1}
     # hist r + scatter r/w (MSD path only) + K5a split count r + scatter r/w (split buckets) + tile sort r/w + merge levels
     path_bytes = ksize * cfg.n * (2 if shared else 5) + 3 * ksize * m_split + sum(level_bytes)
-    if pairs:  # pack (r 4 + w 8), tag copy (r 8 + w 8), unpack (r 8 + tag gather 8 + w 4 + w 8)
+    if pairs and not kv:  # pack (r 4 + w 8), tag copy (r 8 + w 8), unpack (r 8 + tag gather 8 + w 4 + w 8)
         path_bytes += cfg.n * (12 + 16 + 28)
+    elif kv:  # pack (r 8 + 8, w 16), unpack (r 16, w 8 + 8)
+        path_bytes += cfg.n * (32 + 32)
     step_roof = {"alg_bytes_per_step": path_bytes, "bytes_per_key": path_bytes / cfg.n,
                  "t_roof_ms": path_bytes / (peak * 1e9) * 1e3,
                  "frac": path_bytes / (peak * 1e9) / (ms * 1e-3), "levels": max(levels),
@@ -427,7 +434,8 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n_per_gpu": cfg.n, "num_digits": cfg.num_digits,
                        "api": ("hs_sort_shared (no MSD step, SURVEY f1)" if shared else
-                               "hs_sort_pairs (int32 key + 64-bit tag items, stable; SURVEY f3)" if pairs else
+                               ("hs_sort_pairs64 (int64 key + 64-bit tag items on the stable KV path; SURVEY f3)" if kv
+                                else "hs_sort_pairs (int32 key + 64-bit tag items, stable; SURVEY f3)") if pairs else
                                "hs_sort replayed from a CUDA graph (SortGraph)" if graph is not None else "hs_sort"),
                        "chunks_per_bucket": cfg.chunks, "merge_levels": max(levels),
                        "parallelism": "replicas" if world > 1 else "single GPU",

@@ -283,7 +283,7 @@ int hs_abi_version(void);
  * keys per scatter tile, per tile-sort tile and per merge CTA for dtype.
  */
 int hs_last_launch_count(void);
-int hs_tile_keys(hs_dtype_t dtype, int which /* 0 scatter, 1 tile sort, 2 merge */);
+int hs_tile_keys(hs_dtype_t dtype, int which /* 0 scatter, 1 tile sort, 2 merge, 3 f3 item tile sort */);
 
 /*
  * Per-kernel timing (bench only): while enabled on the calling host thread,

@@ -395,6 +395,7 @@ int hs_last_launch_count(void) { return g_launches; }
 int hs_tile_keys(hs_dtype_t dtype, int which) {
     if (dtype != HS_INT32 && dtype != HS_INT64) return 0;
     const int dt = (int)dtype;
+    if (which == 3) return hs::kv_tile_keys();  // tile-sort capacity of the f3 item path (either key dtype)
     return which == 0 ? hs::scatter_tile_keys(dt) : which == 1 ? hs::sort_tile_keys(dt) : hs::merge_span(dt);
 }
 
