@@ -353,8 +353,8 @@ def run_ours(args, cfg):
     peak, peak_src = peaks()
     achieved = per_kernel[dom].get("alg_GBps")
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
-    if os.path.exists(tp):
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")  # ncu capture of hs_sort on this config
+    if os.path.exists(tp) and not (shared or pairs):
         with open(tp) as f:
             traffic = json.load(f).get(dom)
     active = [b for b in level_bytes if b > 0]
