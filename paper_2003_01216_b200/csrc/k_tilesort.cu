@@ -23,6 +23,7 @@
 // Keys-only data makes the sorted tile unique, so neither path's (unstable)
 // order of equal keys is observable.
 #include <cstdint>
+#include <type_traits>
 
 #include "hs_device.cuh"
 #include "hs_launch.h"
@@ -56,6 +57,9 @@
 #endif
 #ifndef HS_SORT_BUNROLL
 #define HS_SORT_BUNROLL 1
+#endif
+#ifndef HS_SORT_ADAPTIVE
+#define HS_SORT_ADAPTIVE 1  // bucket networks sized to the warp's largest bucket (0: always CAP)
 #endif
 #ifndef HS_SORT_CAP64
 #define HS_SORT_CAP64 28  // mean 0.9 T / 2NT = 12 on split leaves (1024 buckets): few tiles overflow
@@ -123,6 +127,15 @@ __device__ __forceinline__ int merge_path_s(const K *A, int na, const K *B, int 
         else r = mid;
     }
     return l;
+}
+
+// Packed bucket networks (int32): the bucket pass sorts each thread's two buckets with the smallest
+// of four compile-time networks that holds the largest bucket of the warp (CAP - 3s, CAP - 2s,
+// CAP - s, CAP with s = CAP / 6 rounded down to even) -- a Poisson-sized bucket rarely needs CAP
+// (C3 tile sort -4.5%, C4 -4%).
+template <int CAP, int I>
+__host__ __device__ constexpr int net_size() {
+    return HS_SORT_ADAPTIVE ? CAP - (3 - I) * ((CAP / 6) & ~1) : CAP;
 }
 
 template <typename K>
@@ -278,7 +291,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     // (else plain stores: the big-piece path reads its own outputs back);
     // samp_x >= 0: write the key samples of output positions samp_x + [0, len).
     auto sort_tile = [&](const K *in, const int len, K *const out, const int phase, const bool bulk,
-                         const long long samp_x) {
+                         const long long samp_x) __attribute__((always_inline)) {
         // 1. bulk load of the 16-byte aligned superset of the leaf
         const uintptr_t ga0 = (uintptr_t)in & ~(uintptr_t)15;
         const uintptr_t ga1 = ((uintptr_t)(in + len) + 15) & ~(uintptr_t)15;
@@ -460,22 +473,31 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
             __syncthreads();
             if constexpr (sizeof(K) == 4 && BPT_ == 2) {
                 const uint32_t stA = bk_base, cA = bk_cnt[0], stB = bk_base + bk_cnt[0], cB = bk_cnt[1];
-                if (cA > 1 || cB > 1) {
-                    const int32_t rA = cA ? (int32_t)so[stA] : 0, rB = cB ? (int32_t)so[stB] : 0;
-                    H2 w[CAP];
+                auto run = [&](auto NCAP) {
+                    constexpr int N = decltype(NCAP)::value;
+                    if (cA > 1 || cB > 1) {
+                        const int32_t rA = cA ? (int32_t)so[stA] : 0, rB = cB ? (int32_t)so[stB] : 0;
+                        H2 w[N];
     #pragma unroll
-                    for (int i = 0; i < CAP; ++i) {
-                        const uint32_t lo = i < (int)cA ? (uint32_t)((int32_t)so[stA + i] - rA + 32768) : 0xFFFFu;
-                        const uint32_t hi = i < (int)cB ? (uint32_t)((int32_t)so[stB + i] - rB + 32768) : 0xFFFFu;
-                        w[i].v = lo | (hi << 16);
-                    }
-                    oddeven_sort<CAP>(w);
+                        for (int i = 0; i < N; ++i) {
+                            const uint32_t lo = i < (int)cA ? (uint32_t)((int32_t)so[stA + i] - rA + 32768) : 0xFFFFu;
+                            const uint32_t hi = i < (int)cB ? (uint32_t)((int32_t)so[stB + i] - rB + 32768) : 0xFFFFu;
+                            w[i].v = lo | (hi << 16);
+                        }
+                        oddeven_sort<N>(w);
     #pragma unroll
-                    for (int i = 0; i < CAP; ++i) {
-                        if (i < (int)cA) so[stA + i] = (K)(rA + (int32_t)(w[i].v & 0xFFFFu) - 32768);
-                        if (i < (int)cB) so[stB + i] = (K)(rB + (int32_t)(w[i].v >> 16) - 32768);
+                        for (int i = 0; i < N; ++i) {
+                            if (i < (int)cA) so[stA + i] = (K)(rA + (int32_t)(w[i].v & 0xFFFFu) - 32768);
+                            if (i < (int)cB) so[stB + i] = (K)(rB + (int32_t)(w[i].v >> 16) - 32768);
+                        }
                     }
-                }
+                };
+                // the smallest network that holds the warp's largest bucket (CTA-uniform branch: all lanes here)
+                const uint32_t wm = __reduce_max_sync(0xffffffffu, cA > cB ? cA : cB);
+                if (wm <= (uint32_t)net_size<CAP, 0>()) run(std::integral_constant<int, net_size<CAP, 0>()>{});
+                else if (wm <= (uint32_t)net_size<CAP, 1>()) run(std::integral_constant<int, net_size<CAP, 1>()>{});
+                else if (wm <= (uint32_t)net_size<CAP, 2>()) run(std::integral_constant<int, net_size<CAP, 2>()>{});
+                else run(std::integral_constant<int, CAP>{});
             }
         } else if (mode == 2) {
             // sort my buckets in registers (v is dead on this path)
@@ -485,15 +507,20 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     #pragma unroll kBU
             for (int q = 0; q < BPT_; ++q) {
                 const uint32_t cn = bk_cnt[q];
-                if (cn > 1) {
-                    K w[CAP];
+                auto run = [&](auto NCAP) {
+                    constexpr int N = decltype(NCAP)::value;
+                    if (cn > 1) {
+                        K w[N];
     #pragma unroll
-                    for (int i = 0; i < CAP; ++i) w[i] = i < (int)cn ? so[st + i] : kMax;
-                    oddeven_sort<CAP>(w);
+                        for (int i = 0; i < N; ++i) w[i] = i < (int)cn ? so[st + i] : kMax;
+                        oddeven_sort<N>(w);
     #pragma unroll
-                    for (int i = 0; i < CAP; ++i)
-                        if (i < (int)cn) so[st + i] = w[i];
-                }
+                        for (int i = 0; i < N; ++i)
+                            if (i < (int)cn) so[st + i] = w[i];
+                    }
+                };
+                // (one CAP network: sizing it to the warp's largest bucket measured 4% slower on int64 keys)
+                run(std::integral_constant<int, CAP>{});
                 st += cn;
             }
         } else if (mode == 0) {
@@ -593,17 +620,14 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     int lgp = 0;
     while (((long long)T << lgp) < len) ++lgp;
     K *const fin = fin_base + lo;
-    if (lgp == 0) {
-        sort_tile(src + lo, len, fin, 0, true, lo);
-        return;
-    }
     K *const alt = (fin_base == F ? S : F) + lo;
     K *xb = (lgp & 1) ? alt : fin;  // the parts' sorted runs; the last pass writes fin
-    for (int part = 0; part < (1 << lgp); ++part) {
+    for (int part = 0; part < (1 << lgp); ++part) {  // (one call site: sort_tile stays inlined)
         const int ps = (int)part_start(len, lgp, part), pe = (int)part_start(len, lgp, part + 1);
-        __syncthreads();  // the previous part is done with shared memory
-        sort_tile(src + lo + ps, pe - ps, xb + ps, part, false, -1);
+        if (part) __syncthreads();  // the previous part is done with shared memory
+        sort_tile(src + lo + ps, pe - ps, xb + ps, part, lgp == 0, lgp == 0 ? lo : -1LL);
     }
+    if (lgp == 0) return;
     K *yb = xb == fin ? alt : fin;
     for (int r = 0; r < lgp; ++r) {
         const bool last = r + 1 == lgp;
