@@ -30,7 +30,7 @@ namespace hs {
 #define HS_KV_NT 256
 #endif
 #ifndef HS_KV_VT
-#define HS_KV_VT 11
+#define HS_KV_VT 15
 #endif
 
 // ----------------------------------------------------------------- pack / unpack

@@ -134,11 +134,14 @@ def assert_same(got, ref, what):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,distinct,c", [(0, 1, 8), (1, 1, 8), (5, 2, 2), (2815, 40, 8), (2817, 40, 8),
-                                          (100_003, 1000, 8), (400_001, 50, 16), (1_000_003, 10**9, 8),
-                                          (300_007, 3, 1)])
+@pytest.mark.parametrize("n,distinct,c", [(0, 1, 8), (1, 1, 8), (5, 2, 2), ("T-1", 40, 1), ("T+1", 40, 1),
+                                          ("8T+3", 40, 8), (100_003, 1000, 8), (400_001, 50, 16),
+                                          (1_000_003, 10**9, 8), (300_007, 3, 1)])
 def test_sort_pairs64_parity(n, distinct, c):
     torch, hs = _gpu()
+    if isinstance(n, str):  # around the item tile size (K5kv leaves)
+        t = hs.tile_keys(1, 3)
+        n = {"T-1": t - 1, "T+1": t + 1, "8T+3": 8 * t + 3}[n]
     g = np.random.default_rng(n + distinct)
     vals = g.integers(0, 10**18, size=min(distinct, 10**6), dtype=np.int64)
     keys = vals[g.integers(0, vals.size, size=n)] if distinct < 10**9 else g.integers(0, 10**18, size=n)

@@ -93,8 +93,14 @@ def run(names, cfg_name="C3", reps=5):
         dt = 0 if src.dtype == torch.int32 else 1
         stream = torch.cuda.current_stream().cuda_stream
 
+        tags = torch.arange(buf.numel(), dtype=torch.int64, device=buf.device)
+
         def call():
-            rc = lib.hs_sort(buf.data_ptr(), buf.numel(), dt, cfg.num_digits, cfg.chunks, stream)
+            if os.environ.get("EXP_PAIRS"):
+                rc = lib.hs_sort_pairs64(buf.data_ptr(), tags.data_ptr(), buf.numel(), cfg.num_digits, cfg.chunks,
+                                         stream)
+            else:
+                rc = lib.hs_sort(buf.data_ptr(), buf.numel(), dt, cfg.num_digits, cfg.chunks, stream)
             assert rc == 0, lib.hs_last_error_message()
         for _ in range(2):
             buf.copy_(src); call()
