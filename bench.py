@@ -493,24 +493,47 @@ def run_dist(args, cfg):
     buf = torch.empty_like(src)
     times = []
     info = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    sampler = ClockSampler(local)
+
+    def step():
+        if args.fused:
+            return hd.dist_sort_fused(buf, cfg.num_digits, cfg.chunks)
+        return hd.dist_sort(buf, cfg.num_digits, cfg.chunks)
+
+    with sampler:
+        for i in range(args.warmup + args.steps):
+            buf.copy_(src)
+            flush.fill_(1)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out, info = step()
+            b.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                times.append(a.elapsed_time(b))
+    launches = hs.last_launch_count()  # the local sort's kernels of the last step (plus K1-K3 on the fused path)
+    ms = statistics.mean(times)
+    # e2e: this rank's keys pinned host -> device, the distributed sort, its sorted piece device -> pinned host
+    e2e_ms = []
     for i in range(args.warmup + args.steps):
-        buf.copy_(src)
         dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        if args.fused:
-            out, info = hd.dist_sort_fused(buf, cfg.num_digits, cfg.chunks)
-        else:
-            out, info = hd.dist_sort(buf, cfg.num_digits, cfg.chunks)
+        buf.copy_(h, non_blocking=True)
+        out, info = step()
+        h_out = torch.empty(out.numel(), dtype=out.dtype, pin_memory=True)
+        h_out.copy_(out, non_blocking=True)
         b.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
-            times.append(a.elapsed_time(b))
-    ms = statistics.mean(times)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            e2e_ms.append(a.elapsed_time(b))
+    t = torch.tensor([ms, statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms, e2e = float(t[0].item()), float(t[1].item())
     ok = bool(torch.all(out[1:] >= out[:-1]).item()) if out.numel() > 1 else True
     if rank == 0:
         line = {"metric": METRIC, "value": world * cfg.n / (ms * 1e-3) / 1e9, "unit": "Gkeys/s", "n_gpus": world,
@@ -521,8 +544,16 @@ def run_dist(args, cfg):
                                            f"symmetric memory): {world} ranks (SURVEY f2, P:78-80)" if args.fused else
                                            f"bucket sharding over NCCL all-to-all-v: {world} ranks (SURVEY f2, P:78-80)"),
                            "group_start": info.group_start, "max_group_keys": info.max_load,
+                           "l2": "flushed (256 MiB device write) before every timed step",
                            "timing": "CUDA events around dist_sort (partition, size all-gather, all-to-all-v, "
                                      "local hs_sort), max over ranks"},
+                "e2e": {"value": world * cfg.n / (e2e * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": e2e,
+                        "h2d_bytes_per_step": world * cfg.n * h.element_size(),
+                        "d2h_bytes_per_step": world * cfg.n * h.element_size(),
+                        "how": "per rank: pinned H2D of its keys, the distributed sort, D2H of its sorted piece; "
+                               "CUDA events, max over ranks"},
+                "gpu_launches": launches * args.steps,
+                "clocks": sampler.result(),
                 "sorted_check": ok}
         print(json.dumps(line), flush=True)
     dist.barrier()

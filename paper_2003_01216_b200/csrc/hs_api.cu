@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "hs.h"
+#include <nvtx3/nvToolsExt.h>
 #include "hs_device.cuh"
 #include "hs_launch.h"
 
@@ -24,6 +25,14 @@
 #endif
 
 namespace {
+
+// NVTX range around every entry point that enqueues work (header-only NVTX3: a
+// no-op unless a profiler such as nsys / ncu --nvtx is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define HS_NVTX(name) NvtxRange hs_nvtx_range_(name)
 
 thread_local char g_err[512] = "";
 thread_local int g_launches = 0;         // kernels of the last successful call (hs_last_launch_count)
@@ -435,6 +444,7 @@ extern "C" {
 
 hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int64_t *bucket_offsets,
                              void *out, cudaStream_t stream) {
+    HS_NVTX("hs_msd_partition");
     hs_status_t s;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
     if ((s = check_digits(num_digits, dtype)) != HS_OK) return s;
@@ -543,6 +553,7 @@ extern "C" {
 
 hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                     cudaStream_t stream) {
+    HS_NVTX("hs_sort");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -561,6 +572,7 @@ hs_status_t hs_sort(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int
 
 hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, const int64_t *bucket_offsets,
                             int chunks_per_bucket, cudaStream_t stream) {
+    HS_NVTX("hs_sort_buckets");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -583,6 +595,7 @@ hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_dig
 
 hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                          int32_t *levels_out, int32_t *split_out, int32_t *leaves_out, cudaStream_t stream) {
+    HS_NVTX("hs_sort_plan");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -620,6 +633,7 @@ struct hs_partition_plan_s {
 
 hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits,
                                      int64_t *bucket_offsets, hs_partition_plan_t *plan, cudaStream_t stream) {
+    HS_NVTX("hs_partition_plan_create");
     hs_status_t s;
     if (!plan) return fail(HS_ERR_INVALID_VALUE, "plan is NULL");
     *plan = nullptr;
@@ -659,6 +673,7 @@ hs_status_t hs_partition_plan_create(const void *keys, int64_t n, hs_dtype_t dty
 }
 
 hs_status_t hs_partition_scatter(hs_partition_plan_t plan, void *const *dst, cudaStream_t stream) {
+    HS_NVTX("hs_partition_scatter");
     if (!plan || !dst) return fail(HS_ERR_INVALID_VALUE, "plan or dst is NULL");
     const int ks = ksize(plan->dtype);
     for (int d = 0; d < 10; ++d)
@@ -684,6 +699,7 @@ hs_status_t hs_partition_plan_destroy(hs_partition_plan_t plan, cudaStream_t str
 hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, int64_t n, int num_digits,
                                    int64_t *bucket_offsets, int32_t *out_keys, uint64_t *out_tags,
                                    cudaStream_t stream) {
+    HS_NVTX("hs_msd_partition_pairs");
     hs_status_t s;
     if ((s = check_common(n, HS_INT32)) != HS_OK) return s;
     if ((s = check_digits(num_digits, HS_INT32)) != HS_OK) return s;
@@ -725,6 +741,7 @@ hs_status_t hs_msd_partition_pairs(const int32_t *keys, const uint64_t *tags, in
 
 hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
                           cudaStream_t stream) {
+    HS_NVTX("hs_sort_pairs");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, HS_INT32)) != HS_OK) return s;
@@ -770,6 +787,7 @@ hs_status_t hs_sort_pairs(int32_t *keys, uint64_t *tags, int64_t n, int num_digi
 }
 
 hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, cudaStream_t stream) {
+    HS_NVTX("hs_sort_shared");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -806,6 +824,7 @@ hs_status_t hs_sort_shared(void *keys, int64_t n, hs_dtype_t dtype, int chunks, 
 
 hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
                            int chunks_per_bucket, cudaStream_t stream) {
+    HS_NVTX("hs_sort_chunks");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -845,6 +864,7 @@ hs_status_t hs_sort_chunks(const void *in, void *out, int64_t n, hs_dtype_t dtyp
 
 hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets,
                      int chunks_per_bucket, cudaStream_t stream) {
+    HS_NVTX("hs_merge");
     hs_status_t s;
     int log2c;
     if ((s = check_common(n, dtype)) != HS_OK) return s;
@@ -1006,6 +1026,7 @@ extern "C" {
 
 hs_status_t hs_sort_pairs64(int64_t *keys, uint64_t *tags, int64_t n, int num_digits, int chunks_per_bucket,
                             cudaStream_t stream) {
+    HS_NVTX("hs_sort_pairs64");
     hs_status_t s;
     int log2c;
     if ((s = check_kv_args(keys, tags, keys, tags, n, HS_INT64, true)) != HS_OK) return s;
@@ -1022,6 +1043,7 @@ hs_status_t hs_sort_pairs64(int64_t *keys, uint64_t *tags, int64_t n, int num_di
 hs_status_t hs_msd_partition_pairs64(const int64_t *keys, const uint64_t *tags, int64_t n, int num_digits,
                                      int64_t *bucket_offsets, int64_t *out_keys, uint64_t *out_tags,
                                      cudaStream_t stream) {
+    HS_NVTX("hs_msd_partition_pairs64");
     hs_status_t s;
     if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, HS_INT64, false)) != HS_OK) return s;
     if ((s = check_digits(num_digits, HS_INT64)) != HS_OK) return s;
@@ -1073,6 +1095,7 @@ hs_status_t hs_msd_partition_pairs64(const int64_t *keys, const uint64_t *tags, 
 hs_status_t hs_sort_chunks_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags,
                                  int64_t n, hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
                                  cudaStream_t stream) {
+    HS_NVTX("hs_sort_chunks_pairs");
     hs_status_t s;
     int log2c;
     if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, dtype, true)) != HS_OK) return s;
@@ -1090,6 +1113,7 @@ hs_status_t hs_sort_chunks_pairs(const void *keys, const uint64_t *tags, void *o
 hs_status_t hs_merge_pairs(const void *keys, const uint64_t *tags, void *out_keys, uint64_t *out_tags, int64_t n,
                            hs_dtype_t dtype, const int64_t *bucket_offsets, int chunks_per_bucket,
                            cudaStream_t stream) {
+    HS_NVTX("hs_merge_pairs");
     hs_status_t s;
     int log2c;
     if ((s = check_kv_args(keys, tags, out_keys, out_tags, n, dtype, true)) != HS_OK) return s;

@@ -313,6 +313,29 @@ def test_split_density_ramp():
     assert sum(plan["split"]) == 10, plan
 
 
+@pytest.mark.parametrize("c", [2, 8])
+def test_split_big_pieces_int64_and_items(c):
+    """The big-piece path (1-4 tiles per sub-range piece) on int64 keys and on hs_sort_pairs items
+    (the int64 path with key = item >> 32): a dense value range inside one sub-range per chunk."""
+    t, D = T(1), 18
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(77 + c)
+    m = c * 3 * t
+    parts = [rng.integers(b * div, (b + 1) * div, size=m) for b in range(10)]
+    parts.append(rng.integers(5 * div + 10**9, 5 * div + 10**9 + 5 * t, size=int(2.5 * t) * c))
+    keys = np.concatenate(parts).astype(np.int64)
+    rng.shuffle(keys)
+    plan = check(keys, D, c)
+    assert plan["split"][5] == 1, plan
+    k32 = (rng.integers(0, 10**9, size=c * 4 * T(1) * 10) // 1).astype(np.int32)
+    k32[: int(2.5 * T(1)) * c * 3] = 500_000_123 + rng.integers(0, 2000, size=int(2.5 * T(1)) * c * 3)
+    tags = rng.permutation(k32.size).astype(np.uint64)
+    dk, dt = torch.from_numpy(k32).to(DEV), torch.from_numpy(tags.view(np.int64)).to(DEV)
+    hs.hs_sort_pairs(dk, dt, 9, c)
+    rk, rt = O.sort_pairs(k32, tags, 9, c)
+    assert np.array_equal(dk.cpu().numpy(), rk) and np.array_equal(dt.cpu().numpy().view(np.uint64), rt)
+
+
 def test_split_big_pieces_sorted_in_cta():
     """Sub-range pieces of 1-4 tiles (values with ~2.2 T copies per chunk, plus a narrow
     non-constant peak): the bucket keeps the split -- such a piece is sorted by its CTA as tiles +
