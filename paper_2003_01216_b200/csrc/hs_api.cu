@@ -484,7 +484,9 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     digit_params(num_digits, key_shift ? HS_INT64 : dtype, &div, &magic);
 
     // K5a value split of the chunks (compile-time HS_SPLIT, see the top of this file)
-    constexpr bool split_on = HS_SPLIT != 0;
+    // No chunk can exceed one tile when ceil(n / c) <= T (a bucket holds at most n keys), so no bucket
+    // can take the split: its kernels are not launched at all (small n: launch-bound).
+    const bool split_on = HS_SPLIT != 0 && (n + (1LL << log2c) - 1) / (1LL << log2c) > T;
     const long long split_words = split_on ? hs::split_table_words(n, log2c, T) : 0;
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
