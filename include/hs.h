@@ -139,10 +139,12 @@ hs_status_t hs_merge(const void *in, void *out, int64_t n, hs_dtype_t dtype,
  * partition step with many pivots (K5a): the chunk is split by key value into
  * equal-width sub-ranges of its bucket's digit range (or, for a bucket whose
  * sampled key distribution is skewed, equal-count groups of 2048 fine bins),
- * each of which is then sorted in one shared-memory tile; a bucket whose
- * sub-ranges still overflow a tile (a value with more than a tile of copies in
- * a chunk) falls back to tile sort + in-chunk merge levels.  Either way the
- * result is the unique ascending array.  (A build with -DHS_SPLIT=0 omits the
+ * each of which is then sorted in one shared-memory tile (a sub-range piece of
+ * up to 4 tiles -- duplicates, skew -- is sorted by its CTA as tiles + CTA
+ * merges; a piece of any length whose keys are all equal is filled, not
+ * sorted); a bucket with a longer, non-constant piece falls back to tile sort
+ * + in-chunk merge levels.  Either way the result is the unique ascending
+ * array.  (A build with -DHS_SPLIT=0 omits the
  * split, for A/B measurements only; nothing at run time changes the path.)
  *
  *   keys[n]            in/out: device; ascending on return.
