@@ -743,6 +743,7 @@ __global__ void __launch_bounds__(256) k_split_fill(const Ctl *__restrict__ ctl,
         else val = (K)(long long)(u ^ 0x8000000000000000ull);
         K *const o = tile_out + cs + tab[w];
         const long long len = (long long)tab[w + 1] - tab[w];
+        HS_DASSERT(len >= 0 && sc.cflag[w] == 1 && sc.gmax[w] == ~sc.gminc[w]);
         for (long long p = gtid; p < len; p += gstride) o[p] = val;
     }
 }

@@ -192,6 +192,7 @@ __device__ void cta_merge(const K *A, int na, const K *B, int nb, K *O, K *sbuf,
     for (int o = 0; o < n;) {
         const int cnt = min(W, n - o);
         const int la = min(cnt, na - ai), lb = min(cnt, nb - bi);
+        HS_DASSERT(la >= 0 && lb >= 0 && la + lb >= cnt && 3 * W <= T);
         for (int j = tid; j < la; j += NT) sA[j] = A[ai + j];
         for (int j = tid; j < lb; j += NT) sB[j] = B[bi + j];
         __syncthreads();
@@ -207,6 +208,7 @@ __device__ void cta_merge(const K *A, int na, const K *B, int nb, K *O, K *sbuf,
         }
         if (tid == 0) s_adv = merge_path_s(sA, la, sB, lb, cnt);  // A keys consumed by this window
         __syncthreads();
+        HS_DASSERT(s_adv >= 0 && s_adv <= la && cnt - s_adv <= lb);
         for (int j = tid; j < cnt; j += NT) O[o + j] = sO[j];
         if (samp) write_samples(samp, sx + o, cnt, sO, tid, NT);
         ai += s_adv;

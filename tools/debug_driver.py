@@ -91,6 +91,18 @@ def main():
         mk, mt = O.merge_pairs(ck, ct, poff, 4)
         assert np.array_equal(dk.cpu().numpy(), mk) and np.array_equal(dtg.cpu().numpy().view(np.uint64), mt)
         cases += 2
+    # big pieces (1-4 tiles: a dense value range) and constant pieces (one value, ~6 tiles per chunk)
+    t = 27_136
+    for c in (2, 8):
+        keys = W.uniform(c * 12 * t, 5 + c, 10**9, dtype=np.int32)
+        keys[: int(2.5 * t) * c] = 500_000_000 + rng.integers(0, 3 * t, size=int(2.5 * t) * c)
+        keys[int(2.5 * t) * c: int(8.5 * t) * c] = 300_000_777
+        rng.shuffle(keys)
+        d = torch.from_numpy(keys).to(dev)
+        ok(lib.hs_sort(d.data_ptr(), keys.size, 0, 9, c, st))
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), np.sort(keys)), ("big/constant pieces", c)
+        cases += 1
     # one full-size config through the debug checks
     keys = W.generate("C2")
     d = torch.from_numpy(keys).to(dev)
