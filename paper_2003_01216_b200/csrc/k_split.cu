@@ -104,7 +104,7 @@ struct SplitConst {
     unsigned long long *gminc;  // ~u(min) per split-table word
     unsigned long long *gmax;   // u(max)
     uint32_t *cflag;            // 1: constant piece
-    unsigned long long *clist;  // constant pieces (split-table word, absolute chunk start), C.nconst of them
+    unsigned long long *clist;  // constant pieces (split-table word, absolute chunk start, bucket), C.nconst of them
 };
 __device__ __forceinline__ unsigned long long ukey(int32_t k) { return (unsigned long long)((uint32_t)k ^ 0x80000000u); }
 __device__ __forceinline__ unsigned long long ukey(int64_t k) { return (unsigned long long)k ^ 0x8000000000000000ull; }
@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(256) k_split_fill(const Ctl *__restrict__ ctl,
     const unsigned nc = ctl->split.nconst;
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x, gstride = (long long)gridDim.x * blockDim.x;
     for (unsigned i = 0; i < nc; ++i) {
-        const long long w = (long long)sc.clist[2 * i], cs = (long long)sc.clist[2 * i + 1];
+        // a bucket that still fell back (another piece over the limit and not constant) keeps its
+        // partitioned keys where tile_out may point: its constant pieces are not filled
+        if (!ctl->plan.split[sc.clist[3 * i + 2]]) continue;
+        const long long w = (long long)sc.clist[3 * i], cs = (long long)sc.clist[3 * i + 1];
         const unsigned long long u = sc.gmax[w];
         K val;
         if constexpr (sizeof(K) == 4) val = (K)(int32_t)((uint32_t)u ^ 0x80000000u);
@@ -772,8 +775,9 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
             if (C.cc[b] && sc.gmax[rb + q] == ~sc.gminc[rb + q]) {
                 sc.cflag[rb + q] = 1;
                 const unsigned slot = atomicAdd(&C.nconst, 1u);  // k_split_fill's work list
-                sc.clist[2 * slot] = (unsigned long long)(rb + q);
-                sc.clist[2 * slot + 1] = (unsigned long long)(P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j));
+                sc.clist[3 * slot] = (unsigned long long)(rb + q);
+                sc.clist[3 * slot + 1] = (unsigned long long)(P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j));
+                sc.clist[3 * slot + 2] = (unsigned long long)b;
             } else {
                 over = true;
             }
@@ -833,7 +837,7 @@ SplitConst split_const(uint32_t *cur, long long tab_words) {
     return sc;
 }
 
-long long split_cur_words(long long tab_words) { return 10 * ((tab_words + 1) & ~1LL); }
+long long split_cur_words(long long tab_words) { return 12 * ((tab_words + 1) & ~1LL); }
 
 long long split_table_words(long long n, int log2c, int tile_keys) {
     return n / split_target_map(tile_keys) + 40 * (1LL << log2c) + 64 + split_extra_words(log2c);

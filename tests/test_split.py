@@ -371,3 +371,22 @@ def test_split_constant_pieces(dtype, D):
     rng.shuffle(keys)
     plan = check(keys, D, c)
     assert plan["split"][3] == 1 and plan["split"][6] == 1, plan
+
+
+def test_split_constant_piece_in_a_bucket_that_falls_back():
+    """Bucket 3, c = 2: chunk 0's heavy sub-range piece is one value (6 tiles: constant, legal), chunk
+    1's is the same value plus other keys of that sub-range (6.1 tiles, not constant: the bucket falls
+    back).  The constant piece must then NOT be filled (the fill would overwrite the fallback's
+    partitioned keys); exact either way."""
+    t, D, c = T(0), 9, 2
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(4321)
+    heavy = 3 * div + 777
+    others = lambda m: rng.integers(3 * div + div // 8, 4 * div, size=m)   # outside the heavy sub-range
+    chunk0 = np.concatenate([np.full(6 * t, heavy), others(2 * t)])
+    chunk1 = np.concatenate([np.full(6 * t, heavy), rng.integers(3 * div, 3 * div + 1000, size=t // 10),
+                             others(2 * t - t // 10)])
+    rest = np.concatenate([rng.integers(b * div, (b + 1) * div, size=3 * t) for b in range(10) if b != 3])
+    keys = np.concatenate([chunk0, chunk1, rest]).astype(np.int32)   # bucket 3 in this order: chunk 0 then 1
+    plan = check(keys, D, c)
+    assert plan["split"][3] == 0, plan
