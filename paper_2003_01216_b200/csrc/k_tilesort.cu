@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     // (else plain stores: the big-piece path reads its own outputs back);
     // samp_x >= 0: write the key samples of output positions samp_x + [0, len).
     auto sort_tile = [&](const K *in, const int len, K *const out, const int phase, const bool bulk,
-                         const long long samp_x) __attribute__((always_inline)) {
+                         const long long samp_x) {
         // 1. bulk load of the 16-byte aligned superset of the leaf
         const uintptr_t ga0 = (uintptr_t)in & ~(uintptr_t)15;
         const uintptr_t ga1 = ((uintptr_t)(in + len) + 15) & ~(uintptr_t)15;
@@ -622,14 +622,20 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     int lgp = 0;
     while (((long long)T << lgp) < len) ++lgp;
     K *const fin = fin_base + lo;
+    // Two call sites on purpose: sort_tile is then compiled out of line, with
+    // its own register allocation -- measured 1.05 ms vs 1.16 ms for the
+    // inlined single-site form on C3's K5 (profiles/r02/README.md).
+    if (lgp == 0) {
+        sort_tile(src + lo, len, fin, 0, true, lo);
+        return;
+    }
     K *const alt = (fin_base == F ? S : F) + lo;
     K *xb = (lgp & 1) ? alt : fin;  // the parts' sorted runs; the last pass writes fin
-    for (int part = 0; part < (1 << lgp); ++part) {  // (one call site: sort_tile stays inlined)
+    for (int part = 0; part < (1 << lgp); ++part) {
         const int ps = (int)part_start(len, lgp, part), pe = (int)part_start(len, lgp, part + 1);
-        if (part) __syncthreads();  // the previous part is done with shared memory
-        sort_tile(src + lo + ps, pe - ps, xb + ps, part, lgp == 0, lgp == 0 ? lo : -1LL);
+        __syncthreads();  // the previous part is done with shared memory
+        sort_tile(src + lo + ps, pe - ps, xb + ps, part, false, -1);
     }
-    if (lgp == 0) return;
     K *yb = xb == fin ? alt : fin;
     for (int r = 0; r < lgp; ++r) {
         const bool last = r + 1 == lgp;
