@@ -38,7 +38,7 @@
 #define HS_SORT_MINB 2
 #endif
 #ifndef HS_SORT_NT64
-#define HS_SORT_NT64 512
+#define HS_SORT_NT64 256  // int64: 128 registers for the bucket networks (512 threads: spills, C5 9.05 vs 7.52 ms)
 #endif
 #ifndef HS_SORT_VT64
 #define HS_SORT_VT64 27
@@ -61,8 +61,11 @@
 #ifndef HS_SORT_ADAPTIVE
 #define HS_SORT_ADAPTIVE 1  // bucket networks sized to the warp's largest bucket (0: always CAP)
 #endif
+#ifndef HS_SORT_RANK64
+#define HS_SORT_RANK64 1  // int64 bucket networks on 32-bit ranks (see the mode-2 loop)
+#endif
 #ifndef HS_SORT_CAP64
-#define HS_SORT_CAP64 28  // mean 0.9 T / 2NT = 12 on split leaves (1024 buckets): few tiles overflow
+#define HS_SORT_CAP64 28  // mean 0.9 T / 2NT = 12 on split leaves (2 NT buckets): few tiles overflow
 #endif
 
 namespace hs {
@@ -133,6 +136,8 @@ __device__ __forceinline__ int merge_path_s(const K *A, int na, const K *B, int 
 // of four compile-time networks that holds the largest bucket of the warp (CAP - 3s, CAP - 2s,
 // CAP - s, CAP with s = CAP / 6 rounded down to even) -- a Poisson-sized bucket rarely needs CAP
 // (C3 tile sort -4.5%, C4 -4%).
+__host__ __device__ constexpr int ilog2_c(int x) { return x <= 1 ? 0 : 1 + ilog2_c(x >> 1); }
+
 template <int CAP, int I>
 __host__ __device__ constexpr int net_size() {
     return HS_SORT_ADAPTIVE ? CAP - (3 - I) * ((CAP / 6) & ~1) : CAP;
@@ -149,10 +154,6 @@ __device__ __forceinline__ void bulk_s2g_ts(void *dst, const void *src, uint32_t
                  : "memory");
 }
 
-__device__ __forceinline__ uint32_t mulhi_u(uint32_t a, uint32_t b) { return __umulhi(a, b); }
-__device__ __forceinline__ unsigned long long mulhi_u(unsigned long long a, unsigned long long b) {
-    return __umul64hi(a, b);
-}
 
 template <typename K>
 __device__ __forceinline__ K lds_k(uint32_t a);
@@ -360,12 +361,15 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     #pragma unroll
             for (int j = 0; j < (PACK ? BPT / 2 : BPT); ++j) bcnt[j * NT + tid] = 0;
             __syncthreads();  // (also: every thread has its keys in v; sbuf is free)
-            // bucket of k = mulhi(((k >> sft) - base) * mulA, M2): one integer map for all modes
-            //   frac:  base, mulA = the sub-range's (see above), M2 = BUCKETS (top bits of the fraction)
-            //   exact (range < BUCKETS): base = min, mulA = 2^w / BUCKETS, M2 = BUCKETS -> k - min
-            //   else:  base = min, mulA = 1, M2 = floor((2^w - 1) / (range + 1)) BUCKETS (< BUCKETS, monotone)
+            // bucket of k = top log2(BUCKETS) bits of ((k >> sft) - base) * mulA (w-bit product, no
+            // overflow): one integer map for all modes
+            //   frac:  base, mulA = the sub-range's (see above) (top bits of the fraction)
+            //   exact (range < BUCKETS): base = min, mulA = 2^w / BUCKETS -> k - min
+            //   else:  base = min, mulA = floor((2^w - 1) / (range + 1)) (equal-width, monotone)
             constexpr U WMAX = ~(U)0;
-            U base = f_base, mulA = f_mul, M2 = (U)BUCKETS;
+            static_assert((BUCKETS & (BUCKETS - 1)) == 0, "power-of-two bucket count");
+            constexpr int kBShift = 8 * (int)sizeof(U) - ilog2_c(BUCKETS);
+            U base = f_base, mulA = f_mul;
             int sft = f_sft;
             bool exact = false, constant = false;
             K mn = 0;
@@ -385,10 +389,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 base = (U)mn;
                 sft = 0;
                 if (exact) mulA = (U)(WMAX / (U)BUCKETS + 1);  // 2^w / BUCKETS
-                else {
-                    mulA = 1;
-                    M2 = range == WMAX ? (U)BUCKETS : WMAX / (range + 1) * (U)BUCKETS;
-                }
+                else mulA = range == WMAX ? (U)1 : WMAX / (range + 1);
                 // a bucket spans about (range + 1) / BUCKETS values
                 packed = sizeof(K) == 4 && !exact && range < ((U)1 << 24);
             }
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                 // no sort and have no capacity limit)
                 auto bucket_of_key = [&](K k) -> int {
                     const U x = ((U)(k >> sft) - base) * mulA;
-                    return (int)mulhi_u(x, M2);  // < BUCKETS, non-decreasing in k
+                    return (int)(x >> kBShift);  // < BUCKETS, non-decreasing in k
                 };
                 // returns the bucket's count before this key (its slot when the counters hold starts)
                 auto bump = [&](int bk) -> uint32_t {
@@ -509,6 +510,61 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
     #pragma unroll kBU
             for (int q = 0; q < BPT_; ++q) {
                 const uint32_t cn = bk_cnt[q];
+#if HS_SORT_RANK64
+                if constexpr (sizeof(K) == 8) {
+                    // int64: sort 32-bit ranks instead of the keys (an int64 comparator costs 4x an
+                    // int32 one: tools/probe/ce_probe.cu).  rank = ((k - min) >> s) << 5 | i with s
+                    // the smallest shift that leaves 27 bits for the bucket's span and i < 32 the
+                    // key's slot; ranks are unique, a 32-bit network orders them, and the keys follow
+                    // by a gather.  Keys with equal (k - min) >> s keep slot order, so the gathered
+                    // run is checked; if two such keys came out of order (keys closer than 2^s; never
+                    // for s = 0) an insertion pass in shared memory repairs the nearly sorted run.
+                    // One CAP network (per-warp sizing: more code than it saves here).
+                    constexpr int N = CAP;
+                    static_assert(N <= 32, "5-bit slots");
+                    if (cn > 1) {
+                        // (keys re-read from shared memory: holding them in registers across the
+                        // network measured slower -- register pressure)
+                        K mnb = so[st], mxb = mnb;
+    #pragma unroll
+                        for (int i = 1; i < N; ++i)
+                            if (i < (int)cn) {
+                                const K x = so[st + i];
+                                mnb = x < mnb ? x : mnb;
+                                mxb = x > mxb ? x : mxb;
+                            }
+                        const U span = (U)mxb - (U)mnb;
+                        const int bits = 64 - __clzll((long long)span);
+                        const int s = bits > 27 ? bits - 27 : 0;
+                        uint32_t rk[N];
+    #pragma unroll
+                        for (int i = 0; i < N; ++i)
+                            rk[i] = i < (int)cn ? ((uint32_t)(((U)so[st + i] - (U)mnb) >> s) << 5) | (uint32_t)i
+                                                : 0xFFFFFFFFu;
+                        oddeven_sort<N>(rk);
+                        K r[N];
+                        bool ok = true;
+    #pragma unroll
+                        for (int j = 0; j < N; ++j) {
+                            r[j] = j < (int)cn ? so[st + (rk[j] & 31u)] : kMax;
+                            if (j > 0) ok &= !(r[j] < r[j - 1]);
+                        }
+    #pragma unroll
+                        for (int j = 0; j < N; ++j)
+                            if (j < (int)cn) so[st + j] = r[j];
+                        if (!ok) {
+                            for (int j = 1; j < (int)cn; ++j) {
+                                const K x = so[st + j];
+                                int m = j;
+                                for (; m > 0 && x < so[st + m - 1]; --m) so[st + m] = so[st + m - 1];
+                                so[st + m] = x;
+                            }
+                        }
+                    }
+                    st += cn;
+                    continue;
+                }
+#endif
                 auto run = [&](auto NCAP) {
                     constexpr int N = decltype(NCAP)::value;
                     if (cn > 1) {

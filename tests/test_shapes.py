@@ -50,3 +50,29 @@ def test_shape_parity(name):
     hs.hs_sort(d, D, C)
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy(), O.sort(keys, D, C)), name
+
+
+def _shape64(name):
+    if name == "uniform":
+        return rng.integers(0, 10**18, N)
+    if name == "near-duplicate clusters":
+        # groups of 4 keys within 1000 of each other: inside a K5 bucket spanning > 2^27 values
+        # they share the 32-bit rank's high part, so the rank network leaves them in slot
+        # order and the repair pass must order them (k_tilesort.cu, HS_SORT_RANK64)
+        c = np.repeat(rng.integers(0, 10**18 - 1000, N // 4), 4)
+        return rng.permutation(c + rng.integers(0, 1000, N))
+    if name == "dense core + wide tail":
+        core = 5 * 10**17 + rng.integers(0, 10**6, N // 2)
+        return rng.permutation(np.concatenate([core, rng.integers(0, 10**18, N - N // 2)]))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["uniform", "near-duplicate clusters", "dense core + wide tail"])
+def test_shape_parity_int64(name):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    keys = np.ascontiguousarray(_shape64(name).astype(np.int64))
+    d = torch.from_numpy(keys).to("cuda:0")
+    hs.hs_sort(d, 18, C)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), O.sort(keys, 18, C)), name
