@@ -26,6 +26,9 @@
 #ifndef HS_K3_SBASE
 #define HS_K3_SBASE 1
 #endif
+#ifndef HS_K3_REDIGIT
+#define HS_K3_REDIGIT 1  // int32 K3: the write loop recomputes each staged key's digit (no digit bytes in smem)
+#endif
 #ifndef HS_SCAT_NT
 #define HS_SCAT_NT 128
 #endif
@@ -273,10 +276,16 @@ struct DstTable {
     int use;
 };
 
+// int32 only: a 64-bit digit (umul64hi) costs more than the staged byte (C5 K3 2.18 vs 2.44 ms)
+template <typename K>
+__host__ __device__ constexpr bool k3_redigit() {
+    return HS_K3_REDIGIT && sizeof(K) == 4;
+}
+
 template <typename K, int NT, int VT>
 struct ScatSmem {
     static constexpr int T = NT * VT;
-    static constexpr size_t bytes() { return (size_t)3 * T * sizeof(K) + T; }  // 2 stages + out + digits
+    static constexpr size_t bytes() { return (size_t)3 * T * sizeof(K) + (k3_redigit<K>() ? 0 : T); }  // 2 stages + out (+ digits)
 };
 
 // Rank + re-stage one tile held in `stage` (blocked: thread tid owns slots
@@ -407,7 +416,7 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
                 const int pos = (int)((wsel >> ((d & 1u) * 16)) & 0xFFFFu) + (int)r;
                 HS_DASSERT(pos >= 0 && pos < T_ && d < 10);
                 sOut[pos] = kv[e];
-                sDig[pos] = (uint8_t)d;
+                if constexpr (!k3_redigit<K>()) sDig[pos] = (uint8_t)d;
             }
         }
     }
@@ -416,9 +425,13 @@ __device__ __forceinline__ void scatter_tile(const K *__restrict__ stage, K *__r
     // ten coalesced runs
     const int nvalid = jhi - jlo;
     for (int j = tid; j < nvalid; j += NT) {
-        HS_DASSERT(sDig[j] < 10);
-        if (TABLE) s_dptr[sDig[j]][j] = sOut[j];
-        else out[s_delta[sDig[j]] + j] = sOut[j];
+        const K key = sOut[j];
+        int d;
+        if constexpr (k3_redigit<K>()) d = msd_digit(key, dp);  // recomputed: cheaper than a staged digit byte
+        else d = sDig[j];
+        HS_DASSERT(d >= 0 && d < 10);
+        if (TABLE) s_dptr[d][j] = key;
+        else out[s_delta[d] + j] = key;
     }
 }
 

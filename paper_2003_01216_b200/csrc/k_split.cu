@@ -600,27 +600,25 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
 // one's write-out).  Ranks by shared atomics (the dummy sub-range ns takes the
 // slots past the slice's end), one global atomic per non-empty sub-range
 // claims the slice's span (in flight during the local scan), keys are staged
-// at their slice-local sorted position together with their destination (one
-// 64-bit word for int32 keys), then written in staged order: consecutive
-// threads write consecutive addresses inside a sub-range.
+// at their slice-local sorted position, then written in staged order with
+// their sub-range recomputed: consecutive threads write consecutive addresses
+// inside a sub-range.
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                             K *__restrict__ F, uint32_t *cur, int nsb_cap,
                                                             const uint16_t *map) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int TS = NT * VT;
-    constexpr bool PACK = sizeof(K) == 4;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t wsum[NT / 32];
     __shared__ SliceDesc sd[2];
     uint32_t *const hist = reinterpret_cast<uint32_t *>(smem_raw);  // [nsb_cap + 1]
-    unsigned long long *const comb = reinterpret_cast<unsigned long long *>(
-        smem_raw + (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15));  // [nsb_cap + 1]: span << 32 | local start
-    unsigned char *const stage = reinterpret_cast<unsigned char *>(comb + nsb_cap + 1);
-    unsigned long long *const spk = reinterpret_cast<unsigned long long *>(stage);  // PACK: dst << 32 | key
-    K *const skeys = reinterpret_cast<K *>(stage);                                 // !PACK
-    uint32_t *const sdst = reinterpret_cast<uint32_t *>(skeys + TS);
+    uint32_t *const sstart = reinterpret_cast<uint32_t *>(
+        smem_raw + (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15));  // [nsb_cap + 1]: slice-local starts
+    uint32_t *const sdelta = sstart + (nsb_cap + 1);                   // [nsb_cap + 1]: span - start
+    K *const skeys = reinterpret_cast<K *>(sdelta + (nsb_cap + 1));    // [TS] staged keys
+
     const int tid = threadIdx.x;
     for (int q = tid; q <= nsb_cap; q += NT) hist[q] = 0;
     long long g = blockIdx.x;
@@ -680,26 +678,18 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
         }
         for (int q = tid + NT; q < ns; q += NT) {
             const uint32_t h = hist[q];
-            comb[q] = h ? atomicAdd(&cur[row + q], h) : 0u;
+            sdelta[q] = h ? atomicAdd(&cur[row + q], h) : 0u;
         }
         cta_excl_scan<NT>(hist, ns + 1, wsum);  // hist -> slice-local starts (overlaps the atomics)
         for (int q = tid; q <= ns; q += NT) {
-            const unsigned long long sp = q == tid ? span0 : (q < ns ? comb[q] : 0ull);
-            comb[q] = (sp << 32) | hist[q];
+            const uint32_t sp = q == tid ? span0 : (q < ns ? sdelta[q] : 0u);
+            sstart[q] = hist[q];
+            sdelta[q] = sp - hist[q];  // destination - staging position inside sub-range q (mod 2^32)
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < VT; ++k) {  // dummy slots land in [cnt, TS) and are not written out
-            const unsigned long long c = comb[tr[k] >> 16];
-            const uint32_t rk = tr[k] & 0xFFFFu;
-            const uint32_t p = (uint32_t)c + rk, dst = (uint32_t)(c >> 32) + rk;
-            if constexpr (PACK) {
-                spk[p] = ((unsigned long long)dst << 32) | (uint32_t)v[k];
-            } else {
-                skeys[p] = v[k];
-                sdst[p] = dst;
-            }
-        }
+        for (int k = 0; k < VT; ++k)  // dummy slots land in [cnt, TS) and are not written out
+            skeys[sstart[tr[k] >> 16] + (tr[k] & 0xFFFFu)] = v[k];
         __syncthreads();  // staged; hist is free; the next descriptor is visible
         const SliceDesc &dn = sd[cb ^ 1];
         {
@@ -710,13 +700,24 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
             const int nz = (cn > 0 && dn.ns > ns) ? dn.ns : ns;
             for (int q = tid; q <= nz; q += NT) hist[q] = 0;
         }
+        // written in staged order; each key's sub-range is recomputed (the same map as the
+        // ranking) to find its destination: only keys are staged, 4 (int64: 8) bytes per key
         K *const oc = F + d.cs;
-        for (int p = tid; p < cnt; p += NT) {
-            if constexpr (PACK) {
-                const unsigned long long w = spk[p];
-                oc[(uint32_t)(w >> 32)] = (K)(uint32_t)w;
+        {
+            const long long lo = d.lo;
+            const unsigned long long mul = d.mul, fmul = d.fmul;
+            const uint16_t *const bmap = d.bmap;
+            const int shift = d.shift;
+            if (bmap == nullptr) {
+                for (int p = tid; p < cnt; p += NT) {
+                    const K key = skeys[p];
+                    oc[(uint32_t)p + sdelta[sub_range_of(key, shift, lo, mul, ns)]] = key;
+                }
             } else {
-                oc[sdst[p]] = skeys[p];
+                for (int p = tid; p < cnt; p += NT) {
+                    const K key = skeys[p];
+                    oc[(uint32_t)p + sdelta[__ldg(bmap + fine_bin<K>(key, shift, lo, fmul))]] = key;
+                }
             }
         }
         __syncthreads();  // staging buffer and sd[cb] free
@@ -857,8 +858,8 @@ cudaError_t setup_split_t() {
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
     const size_t sm_count = (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * (sizeof(K) + 1);
-    const size_t sm_scat = (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * 8 +
-                           (size_t)TS * (sizeof(K) + 4);
+    const size_t sm_scat =
+        (((size_t)(kSplitMaxSub + 1) * 4 + 15) & ~(size_t)15) + (size_t)(kSplitMaxSub + 1) * 8 + (size_t)TS * sizeof(K);
     cudaError_t e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count);
     if (e != cudaSuccess) return e;
@@ -887,8 +888,8 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     const int nsb_cap = nsb_bound(n, log2c, tile_keys);
     const size_t sm_count = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * (sizeof(K) + 1);
     const SplitConst sc = split_const(cur, tab_words);
-    const size_t sm_scat = (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 +
-                           (size_t)TS * (sizeof(K) + 4);
+    const size_t sm_scat =
+        (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 + (size_t)TS * sizeof(K);
     auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, false>;
     auto kcc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, true>;
     auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>;
