@@ -335,6 +335,10 @@ def run_ours(args, cfg):
     if pairs:
         ksize = 16 if kv else 8  # KV64 items, or (key << 32 | index) items through the int64 path
     m = np.diff(off_h)
+    if pairs and not kv and prof.get("split_scatter", (0, 0))[1] > 0:  # int32 items: the int64 path's K5a split
+        t64 = hs.tile_keys(1, 1)
+        split = [int(-(-int(m[b]) // cfg.chunks) > t64) for b in range(10)]
+        levels = [cfg.chunks.bit_length() - 1 if split[b] else levels[b] for b in range(10)]
     per_kernel = {}
     for kind, (tot, cnt) in prof.items():
         if cnt:
@@ -347,6 +351,8 @@ def run_ours(args, cfg):
         "tile_hist": ksize * cfg.n, "scatter": 2 * ksize * cfg.n, "tile_sort": 2 * ksize * cfg.n,
         "merge_level": sum(level_bytes), "split_count": ksize * m_split, "split_scatter": 2 * ksize * m_split,
     }
+    if pairs:  # K0 + K8: pack (r 4 + w 8) and unpack (r 8, tag gather 8, w 4 + 8); KV: r 8 + 8, w 16 and back
+        alg["copy"] = cfg.n * (64 if kv else 40)
     for k, d in per_kernel.items():
         if k in alg and d["ms_per_step"] > 0:
             d["alg_GBps"] = alg[k] / (d["ms_per_step"] * 1e-3) / 1e9

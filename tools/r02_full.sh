@@ -14,6 +14,7 @@ python bench.py --api pairs --steps 5 --no-cpu-baseline > $OUT/bench_pairs_C3.js
 python bench.py --api pairs --config C5 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_pairs_C5.json 2> $OUT/bench_pairs_C5.log
 python bench.py --api shared --steps 5 --no-cpu-baseline > $OUT/bench_shared.json 2> $OUT/bench_shared.log
 python tools/quick_time.py C1 C2 C4 P3 > $OUT/quick.txt 2>&1
+python tools/pcie_probe.py > $OUT/pcie.txt 2>&1
 python tools/dist_sweep.py --kernels > $OUT/dist_sweep.txt 2>&1
 grep "\[bench\]" $OUT/*.log | grep "ms/step =" 
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum
