@@ -424,6 +424,26 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e, e2e_serial = float(t[0].item()), float(t[1].item())
 
+    # context only: the library sort torch ships (a CUB radix sort that also returns
+    # int64 indices) on the same device-resident keys, L2 flushed in between -- not a target
+    context = None
+    if world == 1 and not shared and not pairs and not args.no_context:
+        x = src.clone()
+        ts = []
+        for i in range(2 + 5):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            torch.sort(x)
+            b.record(stream)
+            b.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        del x
+        tms = statistics.median(ts)
+        context = {"torch_sort_ms": tms, "torch_sort_gkeys_s": cfg.n / (tms * 1e-3) / 1e9,
+                   "note": "torch.sort (library radix sort; values + int64 indices) on the same keys; context only"}
+
     if rank == 0:
         log(f"[bench] {cfg.name} hs_sort {ms:.3f} ms/step = {value:.2f} Gkeys/s (steps {[round(x, 3) for x in step_ms]}), "
             f"wall {wall:.3f} s; e2e {e2e:.3f} ms/step pipelined, {e2e_serial:.3f} serial (sorted={ok_e2e})")
@@ -465,6 +485,7 @@ def run_ours(args, cfg):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": sampler.result(),
             "sorted_check": ok and ok_e2e,
+            "context": context,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -577,6 +598,7 @@ def main():
     ap.add_argument("--cpu-sample-omp", type=int, default=0, help="keys for the OpenMP oracle (0: the whole workload)")
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-context", action="store_true", help="skip the torch.sort context timing")
     ap.add_argument("--api", default="sort", choices=["sort", "shared", "pairs"])
     ap.add_argument("--dist", action="store_true", help="bucket-sharded multi-GPU sort (SURVEY f2)")
     ap.add_argument("--fused", action="store_true", help="with --dist: exchange fused into the scatter kernel")
