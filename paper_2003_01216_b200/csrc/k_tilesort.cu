@@ -303,6 +303,9 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
             mbar_arrive_expect_tx(&bar, (uint32_t)(ga1 - ga0));
             bulk_g2s(sbuf, (const void *)ga0, (uint32_t)(ga1 - ga0), &bar);
         }
+        // (sbuf re-derived from the shared symbol here: sort_tile is compiled out of line, and a
+        // captured pointer would reach it as a generic address -- LD/ST instead of LDS/STS)
+        K *const sbuf = reinterpret_cast<K *>(smem_raw);
         K *const sm = sbuf + h;  // sm[0 .. len) = the leaf
         mbar_wait(&bar, phase & 1);
         for (int j = len + tid; j < T; j += NT) sm[j] = kMax;
