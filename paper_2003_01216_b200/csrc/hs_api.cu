@@ -166,11 +166,12 @@ struct Workspace {
     void *samp[2] = {nullptr, nullptr};  // key samples (ping-pong by merge level)
     uint32_t *sbtab = nullptr;           // K5a split table (sub-range starts) and cursors
     uint32_t *sbcur = nullptr;
+    void *pad = nullptr;                 // K5a padded layout: one tile-sized region per (chunk, sub-range)
     size_t zero_bytes = 0;
 };
 
 hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t ntiles, size_t corank_words,
-                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0) {
+                     size_t samp_bytes, cudaStream_t st, size_t split_words = 0, size_t pad_bytes = 0) {
     size_t a = round_up(s_bytes, 256) + (s_bytes ? 256 : 0);  // + slack for 16-byte bulk-copy granules
     size_t c = round_up(sizeof(hs::Ctl), 256);
     size_t z = round_up(status_words * 8, 256);
@@ -180,7 +181,8 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
     size_t sp = round_up(samp_bytes, 256);
     size_t sw = round_up(split_words * 4, 256);
     size_t swc = split_words ? round_up((size_t)hs::split_cur_words((long long)split_words) * 4, 256) : 0;
-    size_t total = a + c + z + th + tp + k + 2 * sp + sw + swc;
+    size_t pb = round_up(pad_bytes, 256);
+    size_t total = a + c + z + th + tp + k + 2 * sp + sw + swc + pb;
     void *p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, total, st);
     if (e != cudaSuccess) {
@@ -203,6 +205,7 @@ hs_status_t ws_alloc(Workspace *w, size_t s_bytes, size_t status_words, size_t n
         w->sbtab = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp);
         w->sbcur = (uint32_t *)(b + a + c + z + th + tp + k + 2 * sp + sw);
     }
+    if (pad_bytes) w->pad = b + a + c + z + th + tp + k + 2 * sp + sw + swc;
     w->zero_bytes = c + z;
     return HS_OK;
 }
@@ -488,9 +491,11 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     // can take the split: its kernels are not launched at all (small n: launch-bound).
     const bool split_on = HS_SPLIT != 0 && (n + (1LL << log2c) - 1) / (1LL << log2c) > T;
     const long long split_words = split_on ? hs::split_table_words(n, log2c, T) : 0;
+    const long long pad_keys = split_on ? hs::split_pad_keys(n, log2c, T) : 0;
     Workspace ws;
     if ((s = ws_alloc(&ws, (size_t)n * ksize(dtype) * (inspect ? 2 : 1), (size_t)hs::scan_ctas(ptiles) * 10,
-                      (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words)) != HS_OK)
+                      (size_t)ptiles, (size_t)nblocks + 2, samp_bytes(n, dtype), stream, (size_t)split_words,
+                      (size_t)pad_keys * ksize(dtype))) != HS_OK)
         return s;
     if (inspect) {  // hs_sort_plan: partition + split into scratch, read the plan back
         void *F = (char *)ws.S + round_up((size_t)n * ksize(dtype), 256);
@@ -500,7 +505,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                                       ws.status, nullptr, hs::kPlanSort, log2c, T, sms, true, stream, key_shift);
         if (e2 == cudaSuccess && split_on)
             e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
-                                  F, stream);
+                                  F, ws.pad, pad_keys, stream);
         if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
         cudaError_t fe = cudaFreeAsync(ws.base, stream);
         if (e2 == cudaSuccess) e2 = fe;
@@ -529,12 +534,12 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
     void *const tile_out = (log2c & 1) ? ws.S : keys;
     if (split_on)
         HS_TRY_CUDA(hs::launch_split(dt, ws.ctl, part, spl, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div,
-                                     key_shift, tile_out, stream),
+                                     key_shift, tile_out, ws.pad, pad_keys, stream),
                     "K5a split");
     // a5: leaf-tile sort (part, or spl for split buckets) -> (keys | S) per bucket parity
     HS_TRY_CUDA(hs::launch_tile_sort(dt, plan, part, keys, ws.S, ws.samp[0], tile_bound(n, chunks_per_bucket, T), stream,
                                      ws.sbtab, &ws.ctl->split, spl,
-                                     split_on ? hs::split_cflag(ws.sbcur, split_words) : nullptr),
+                                     split_on ? hs::split_cflag(ws.sbcur, split_words) : nullptr, ws.pad),
                 "K5 tile sort");
     // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
     const int L = level_bound(n, log2c, T, 1, 1);

@@ -187,7 +187,22 @@ struct SplitCfg {
     unsigned ticket;
     unsigned nconst;             // constant pieces listed for k_split_fill
     int shift;                   // sort key of an item = item >> shift (hs_sort_pairs)
+    // padded layout (no count pass): an equal-width bucket without constant tracking gives every
+    // (chunk, sub-range) a fixed region of cap keys in the pad buffer; the scatter's cursors count
+    // the keys, k_split_pad_plan turns the final cursors into the split table (or, if a region
+    // overflowed, sends the bucket back to the tile + merge-level plan)
+    int pad[10];                 // setup: the pad buffer has room for bucket b (see split_pmode)
+    int k0[10];                  // the leaf plan's k[b] (restored by a padded bucket that overflows)
+    long long pboff[10];         // bucket b's regions start here in the pad buffer (keys)
+    int cap;                     // keys per region (one tile)
+    unsigned ticket2;            // k_split_pad_plan's last-CTA ticket
 };
+
+// Padded layout for bucket b: room in the pad buffer, equal-width sub-ranges (the
+// sample found no skew) and no constant tracking.
+__device__ __forceinline__ bool split_pmode(const SplitCfg &C, int b) {
+    return C.pad[b] && !C.mode[b] && !C.cc[b];
+}
 
 enum PlanMode { kPlanSort = 0, kPlanChunks = 1, kPlanMerge = 2 };
 

@@ -48,7 +48,7 @@ struct SplitCfg;
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab = nullptr,
                              const SplitCfg *scfg = nullptr, const void *src_split = nullptr,  // null: F
-                             const uint32_t *cflag = nullptr);
+                             const uint32_t *cflag = nullptr, const void *src_pad = nullptr);
 
 // K5a (k_split.cu): value split of every chunk of the buckets whose chunks
 // exceed one tile: setup (1 thread), count pass over S, per-chunk scan +
@@ -60,9 +60,12 @@ cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F,
 long long split_table_words(long long n, int log2c, int tile_keys);
 long long split_cur_words(long long tab_words);
 const uint32_t *split_cflag(uint32_t *cur, long long tab_words);
+// padbuf (pad_keys keys, may be null): the padded layout's regions (SplitCfg::pad); its keys are
+// the tile sort's input for padded buckets.
+long long split_pad_keys(long long n, int log2c, int tile_keys);
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
                          long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, void *tile_out,
-                         cudaStream_t st);
+                         void *padbuf, long long pad_keys, cudaStream_t st);
 // samp_in: key samples of the level's input runs (kSampleQ stride); samp_out:
 // the samples this level writes for the next one (may be null).
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,

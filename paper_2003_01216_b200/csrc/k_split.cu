@@ -113,7 +113,8 @@ __device__ __forceinline__ unsigned long long ukey(int32_t k) { return (unsigned
 __device__ __forceinline__ unsigned long long ukey(int64_t k) { return (unsigned long long)k ^ 0x8000000000000000ull; }
 
 __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, int key_shift, int tile_keys,
-                              int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab, SplitConst sc) {
+                              int slice_keys, long long tab_cap, int nsb_cap, uint32_t *tab, SplitConst sc,
+                              long long pad_cap) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     __shared__ long long s_words;
     if (threadIdx.x < 32) {  // lane b < 10: bucket b's geometry (64-bit divisions in parallel)
@@ -137,27 +138,35 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
         }
         // table capacity check and prefixes, in bucket order (lane 0, ten steps)
         long long words = cand ? c * (nsa + 1) : 0;
-        long long ac_t = 0, ac_s = 0, acc_t = 0, acc_s = 0;
-        bool ok = cand;
+        long long ac_t = 0, ac_s = 0, acc_t = 0, acc_s = 0, ac_p = 0, acc_p = 0;
+        bool ok = cand, pok = false;
         for (int q = 0; q < 10; ++q) {
             const long long wq = __shfl_sync(0xffffffffu, words, q);
             const long long sq = __shfl_sync(0xffffffffu, cand ? c * spc : 0LL, q);
+            const long long pq = __shfl_sync(0xffffffffu, cand ? c * ns * (long long)tile_keys : 0LL, q);
             const bool cq = __shfl_sync(0xffffffffu, cand ? 1 : 0, q) && acc_t + wq <= tab_cap;
+            const bool pqok = cq && acc_p + pq <= pad_cap;  // padded regions of the equal-width sub-ranges
             if (q == b) {
                 ok = cq;
+                pok = pqok;
                 ac_t = acc_t;
                 ac_s = acc_s;
+                ac_p = acc_p;
             }
             if (cq) {
                 acc_t += wq;
                 acc_s += sq;
             }
+            if (pqok) acc_p += pq;
         }
         if (b < 10) {
             C.cand[b] = ok;
             C.mode[b] = 0;
             C.slice_prefix[b] = ac_s;
             C.cc[b] = 0;
+            C.pad[b] = pok;
+            C.pboff[b] = ac_p;
+            C.k0[b] = P.k[b];
             if (ok) {
                 C.spc[b] = (int)spc;
                 P.nsb[b] = (int)ns;
@@ -178,6 +187,8 @@ __global__ void k_split_setup(Ctl *ctl, unsigned long long div, int key_bits, in
             }
         }
         if (b == 0) {
+            C.cap = tile_keys;
+            C.ticket2 = 0;
             C.slice_prefix[10] = acc_s;
             C.shift = key_shift;
             C.map_chunks = c <= kMapChunksMax ? (int)c : 1;
@@ -454,10 +465,12 @@ __device__ __forceinline__ void cta_excl_scan(uint32_t *a, int n, uint32_t *wsum
 // one thread computes it and the CTA reads it from shared memory.
 struct SliceDesc {
     long long cs, row, lo;  // chunk start (absolute), split-table row, bucket value base
+    long long ocs;          // where the chunk's sub-ranges go: cs, or (padded layout) its first region in the pad buffer
     unsigned long long mul, fmul;
     const uint16_t *bmap;    // sampled sub-range map of the bucket (null: equal width)
     int cnt, ns, shift, a0;  // keys in the slice (0: nothing to do), sub-ranges, item shift, offset in chunk
     int cc;                  // track constant sub-ranges (SplitConst)
+    int pad;                 // padded layout (split_pmode): regions of cap keys, no count pass
 };
 
 // Called by one thread (the fields share a few cache lines, so after the
@@ -467,10 +480,13 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
     const Plan &P = ctl->plan;
     const SplitCfg &C = ctl->split;
     sd.cnt = 0;
+    sd.ns = 0;
     if (g >= C.slice_prefix[10]) return;
     int b = 0;
     while (b < 9 && g >= C.slice_prefix[b + 1]) ++b;
     if (need_split && !P.split[b]) return;  // a bucket that fell back keeps its keys in S
+    const bool pad = split_pmode(C, b);
+    if (!need_split && pad) return;         // the count pass skips padded buckets
     const unsigned r = (unsigned)(g - C.slice_prefix[b]), spc = (unsigned)C.spc[b];  // < 2^31
     const long long j = r / spc, s = r - (unsigned)j * spc;
     const long long m = P.off[b + 1] - P.off[b];
@@ -478,7 +494,9 @@ __device__ __forceinline__ void slice_desc(SliceDesc &sd, const Ctl *ctl, long l
     const long long a0 = s * TS;
     if (a0 >= c1 - c0) return;
     sd.cnt = (int)((c1 - c0 - a0) < TS ? (c1 - c0 - a0) : TS);
+    sd.pad = pad;
     sd.cs = P.off[b] + c0;
+    sd.ocs = pad ? C.pboff[b] + j * (long long)P.nsb[b] * C.cap : sd.cs;
     sd.a0 = (int)a0;
     sd.ns = P.nsb[b];
     sd.row = P.sboff[b] + j * (P.nsb[b] + 1);
@@ -501,9 +519,11 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
                                                           uint32_t *tab, int nsb_cap, const uint16_t *map,
                                                           SplitConst sc) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
-    if (CC) {
+    {   // exit at once when no bucket needs this pass (CC: constant tracking; else: a counted,
+        // not padded, candidate bucket)
         bool any = false;
-        for (int b = 0; b < 10; ++b) any |= ctl->split.cc[b] != 0;
+        for (int b = 0; b < 10; ++b)
+            any |= CC ? ctl->split.cc[b] != 0 : (ctl->split.cand[b] && !split_pmode(ctl->split, b));
         if (!any) return;
     }
     constexpr int TS = NT * VT;
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
             }
         }
         __syncthreads();  // histogram complete; next descriptor visible
-        if (cc) {
+        if (cc && cnt > 0) {  // (a skipped slice's descriptor has no sub-ranges)
 #pragma unroll 4
             for (int k = 0; k < VT; ++k) {
                 const int t = sub(k);
@@ -609,7 +629,8 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
 template <typename K, int NT, int VT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                             K *__restrict__ F, uint32_t *cur, int nsb_cap,
-                                                            const uint16_t *map) {
+                                                            const uint16_t *map, K *__restrict__ padbuf,
+                                                            int cap_keys) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     constexpr int TS = NT * VT;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
@@ -705,18 +726,31 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
         }
         // written in staged order; each key's sub-range is recomputed (the same map as the
         // ranking) to find its destination: only keys are staged, 4 (int64: 8) bytes per key
-        K *const oc = F + d.cs;
         {
             const long long lo = d.lo;
             const unsigned long long mul = d.mul, fmul = d.fmul;
             const uint16_t *const bmap = d.bmap;
             const int shift = d.shift;
-            if (bmap == nullptr) {
+            if (d.pad) {
+                // padded layout: sub-range t owns [t cap, (t + 1) cap) of the chunk's regions; keys
+                // past a full region are dropped (k_split_pad_plan sees the cursor beyond it and
+                // sends the bucket back to the leaf plan, which reads S)
+                K *const oc = padbuf + d.ocs;
+                const uint32_t cap = (uint32_t)cap_keys;
+                for (int p = tid; p < cnt; p += NT) {
+                    const K key = skeys[p];
+                    const int t = sub_range_of(key, shift, lo, mul, ns);
+                    const uint32_t r = (uint32_t)p + sdelta[t];
+                    if (r < (uint32_t)(t + 1) * cap) oc[r] = key;
+                }
+            } else if (bmap == nullptr) {
+                K *const oc = F + d.ocs;
                 for (int p = tid; p < cnt; p += NT) {
                     const K key = skeys[p];
                     oc[(uint32_t)p + sdelta[sub_range_of(key, shift, lo, mul, ns)]] = key;
                 }
             } else {
+                K *const oc = F + d.ocs;
                 for (int p = tid; p < cnt; p += NT) {
                     const K key = skeys[p];
                     oc[(uint32_t)p + sdelta[__ldg(bmap + fine_bin<K>(key, shift, lo, fmul))]] = key;
@@ -767,7 +801,12 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
     const int lg = P.log2c;
     const int b = blockIdx.x >> lg;
     const long long j = blockIdx.x & ((1 << lg) - 1);
-    if (b < 10 && C.cand[b]) {
+    if (b < 10 && C.cand[b] && split_pmode(C, b)) {
+        // padded layout: nothing was counted; the scatter's cursors start at the regions
+        const int ns = P.nsb[b];
+        uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
+        for (int q = tid; q < ns; q += kSplitPlanNT) crow[q] = (uint32_t)q * (uint32_t)C.cap;
+    } else if (b < 10 && C.cand[b]) {
         const int ns = P.nsb[b];
         uint32_t *row = tab + P.sboff[b] + j * (ns + 1);
         uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
@@ -817,6 +856,68 @@ __global__ void __launch_bounds__(kSplitPlanNT) k_split_plan(Ctl *ctl, uint32_t 
         }
         P.tile_prefix[bb] = acc;
         acc += sp ? c * P.nsb[bb] : (c << P.k[bb]);
+        lmax = P.L[bb] > lmax ? P.L[bb] : lmax;
+    }
+    P.tile_prefix[10] = acc;
+    P.Lmax = lmax;
+}
+
+// ------------------------------------------------------- padded layout plan
+// After the scatter, one CTA per chunk of a padded bucket: the final cursor of
+// region t is t cap + (keys of sub-range t), so the counts come for free; their
+// exclusive scan is the split table row the tile sort reads (where each sorted
+// sub-range goes inside the chunk).  A region whose cursor passed its end
+// (more than a tile of keys: the sample missed a skew) sends the bucket back to
+// the tile + in-chunk merge-level plan -- its keys are still intact in S, and
+// the tile sort then reads them there.  The last CTA re-derives the leaf prefix
+// and Lmax.
+__global__ void __launch_bounds__(kSplitPlanNT) k_split_pad_plan(Ctl *ctl, uint32_t *tab, const uint32_t *cur) {
+    griddep_wait();  // PDL: the scatter's cursor atomics are complete
+    __shared__ uint32_t wsum[kSplitPlanNT / 32];
+    __shared__ bool s_last;
+    Plan &P = ctl->plan;
+    SplitCfg &C = ctl->split;
+    const int tid = threadIdx.x;
+    const int lg = P.log2c;
+    const int b = blockIdx.x >> lg;
+    const long long j = blockIdx.x & ((1 << lg) - 1);
+    if (b < 10 && C.cand[b] && P.split[b] && split_pmode(C, b)) {
+        const int ns = P.nsb[b];
+        uint32_t *row = tab + P.sboff[b] + j * (ns + 1);
+        const uint32_t *crow = cur + P.sboff[b] + j * (ns + 1);
+        const uint32_t cap = (uint32_t)C.cap;
+        bool over = false;
+        for (int q = tid; q < ns; q += kSplitPlanNT) {
+            const uint32_t k = crow[q] - (uint32_t)q * cap;
+            over |= k > cap;
+            row[q] = k;
+        }
+        if (__syncthreads_or(over) && tid == 0) atomicOr(&C.bad, 1u << b);
+        cta_excl_scan<kSplitPlanNT>(row, ns, wsum);
+        if (tid == 0) {
+            const long long m = P.off[b + 1] - P.off[b];
+            row[ns] = (uint32_t)(part_start(m, lg, j + 1) - part_start(m, lg, j));
+            HS_DASSERT(over || row[ns - 1] <= row[ns]);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&C.ticket2, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || tid != 0) return;
+    __threadfence();
+    const unsigned bad = *(volatile unsigned *)&C.bad;
+    const long long c = 1LL << lg;
+    long long acc = 0;
+    int lmax = 0;
+    for (int bb = 0; bb < 10; ++bb) {
+        if (P.split[bb] && ((bad >> bb) & 1u)) {  // a padded bucket that overflowed: the leaf plan
+            P.split[bb] = 0;
+            P.k[bb] = C.k0[bb];
+            P.L[bb] = C.k0[bb] + lg;
+        }
+        P.tile_prefix[bb] = acc;
+        acc += P.split[bb] ? c * P.nsb[bb] : (c << P.k[bb]);
         lmax = P.L[bb] > lmax ? P.L[bb] : lmax;
     }
     P.tile_prefix[10] = acc;
@@ -882,10 +983,32 @@ cudaError_t setup_split_kernels(int dev) {
     return setup_split_t<int64_t>();
 }
 
+// Keys of the pad buffer: c nsb0[b] regions of one tile per bucket, nsb0[b] = ceil(ceil(m_b / c) / 0.9 T)
+// <= (m_b + c) / (0.9 T) + 1, summed over the ten buckets.
+long long split_pad_keys(long long n, int log2c, int tile_keys) {
+    const long long c = 1LL << log2c, t = split_target(tile_keys);
+    return ((n + 10 * c) + t - 1) / t * tile_keys + 10 * c * (long long)tile_keys + 64;
+}
+
+#ifdef HS_DEBUG
+#define HS_SPLIT_STEP(i)                                                             \
+    do {                                                                             \
+        cudaError_t _s = cudaStreamSynchronize(st);                                  \
+        if (_s != cudaSuccess) {                                                     \
+            fprintf(stderr, "HS_DEBUG: K5a step %d: %s\n", i, cudaGetErrorString(_s)); \
+            return _s;                                                               \
+        }                                                                            \
+    } while (0)
+#else
+#define HS_SPLIT_STEP(i) \
+    do {                 \
+    } while (0)
+#endif
+
 template <typename K>
 static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uint32_t *cur, long long tab_words,
                                   long long n, int log2c, int tile_keys, unsigned long long div, int key_shift,
-                                  K *tile_out, cudaStream_t st) {
+                                  K *tile_out, K *padbuf, long long pad_keys, cudaStream_t st) {
     using G = SplGeo<K>;
     constexpr int TS = G::NT * G::VT;
     const int nsb_cap = nsb_bound(n, log2c, tile_keys);
@@ -906,48 +1029,61 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     uint16_t *const map = reinterpret_cast<uint16_t *>(tab + tab_cap);
     prof_begin(kProfPlan, st);
     if ((e = launch_pdl(k_split_setup, dim3(1), dim3(1024), 0, st, ctl, div, 8 * (int)sizeof(K), key_shift,
-                        tile_keys, TS, tab_cap, nsb_cap, tab, sc)) != cudaSuccess)
+                        tile_keys, TS, tab_cap, nsb_cap, tab, sc, padbuf ? pad_keys : 0LL)) != cudaSuccess)
         return e;
+    HS_SPLIT_STEP(0);
     const int mc = (1LL << log2c) <= kMapChunksMax ? (int)(1LL << log2c) : 1;
     if ((e = launch_pdl(k_split_sample_map<K>, dim3(10 * mc), dim3(1024), 0, st, ctl, S, map, tile_keys)) !=
         cudaSuccess)
         return e;
+    HS_SPLIT_STEP(1);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitCount, st);
     const long long pgrid = grid < (long long)sms * G::MINB_COUNT ? grid : (long long)sms * G::MINB_COUNT;
     if ((e = launch_pdl(kc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map, sc)) !=
         cudaSuccess)
         return e;
+    HS_SPLIT_STEP(2);
     if ((e = launch_pdl(kcc, dim3((unsigned)pgrid), dim3(G::NT), sm_count, st, ctl, S, tab, nsb_cap, map, sc)) !=
         cudaSuccess)
         return e;
+    HS_SPLIT_STEP(3);
     prof_end(kProfSplitCount, st);
     prof_begin(kProfPlan, st);
     if ((e = launch_pdl(k_split_plan, dim3((unsigned)(10 * c)), dim3(kSplitPlanNT), 0, st, ctl, tab, cur,
                         tile_keys, sc)) != cudaSuccess)
         return e;
+    HS_SPLIT_STEP(4);
     prof_end(kProfPlan, st);
     prof_begin(kProfSplitScatter, st);
     const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
-    if ((e = launch_pdl(ks, dim3((unsigned)sgrid), dim3(G::NT), sm_scat, st, ctl, S, F, cur, nsb_cap, map)) !=
-        cudaSuccess)
+    if ((e = launch_pdl(ks, dim3((unsigned)sgrid), dim3(G::NT), sm_scat, st, ctl, S, F, cur, nsb_cap, map, padbuf,
+                        tile_keys)) != cudaSuccess)
         return e;
+    HS_SPLIT_STEP(5);
     prof_end(kProfSplitScatter, st);
     prof_begin(kProfPlan, st);
+    if ((e = launch_pdl(k_split_pad_plan, dim3((unsigned)(10 * c)), dim3(kSplitPlanNT), 0, st, ctl, tab,
+                        (const uint32_t *)cur)) != cudaSuccess)
+        return e;
+    HS_SPLIT_STEP(6);
     if ((e = launch_pdl(k_split_fill<K>, dim3((unsigned)(2 * sms)), dim3(256), 0, st, (const Ctl *)ctl,
                         (const uint32_t *)tab, sc, tile_out)) != cudaSuccess)
         return e;
+    HS_SPLIT_STEP(7);
     prof_end(kProfPlan, st);
     return cudaGetLastError();
 }
 
 cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab, uint32_t *cur, long long tab_words,
                          long long n, int log2c, int tile_keys, unsigned long long div, int key_shift, void *tile_out,
-                         cudaStream_t st) {
+                         void *padbuf, long long pad_keys, cudaStream_t st) {
     return dt == 0 ? launch_split_t<int32_t>(ctl, (const int32_t *)S, (int32_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, (int32_t *)tile_out, st)
+                                             tile_keys, div, key_shift, (int32_t *)tile_out, (int32_t *)padbuf,
+                                             pad_keys, st)
                    : launch_split_t<int64_t>(ctl, (const int64_t *)S, (int64_t *)F, tab, cur, tab_words, n, log2c,
-                                             tile_keys, div, key_shift, (int64_t *)tile_out, st);
+                                             tile_keys, div, key_shift, (int64_t *)tile_out, (int64_t *)padbuf,
+                                             pad_keys, st);
 }
 
 const uint32_t *split_cflag(uint32_t *cur, long long tab_words) { return split_const(cur, tab_words).cflag; }

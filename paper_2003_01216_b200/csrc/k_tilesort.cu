@@ -223,7 +223,7 @@ template <typename K, int NT, int VT, int MINB, int BUCKETS, int CAP>
 __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__ plan_g, const K *src, K *F, K *S,
                                                         K *samp, const uint32_t *__restrict__ sbtab,
                                                         const SplitCfg *__restrict__ scfg, const K *src_split,
-                                                        const uint32_t *__restrict__ cflag) {
+                                                        const uint32_t *__restrict__ cflag, const K *src_pad) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
     using G = TSGeo<K, NT, VT>;
@@ -261,6 +261,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
         lo = P.off[b] + part_start(P.off[b + 1] - P.off[b], P.log2c, j) + __ldg(e);
         len = (int)(__ldg(e + 1) - __ldg(e));
         src = src_split;
+        // padded layout (k_split_pad_plan): the sub-range's keys sit at the start of its region
+        if (src_pad && split_pmode(*scfg, b)) src = src_pad + scfg->pboff[b] + (j * ns + t) * scfg->cap - lo;
         if (cflag && __ldg(cflag + (e - sbtab))) {
             // a constant piece (k_split_plan): the scatter already wrote it where this kernel writes;
             // only its key samples are left (every sample is that one key)
@@ -762,14 +764,15 @@ cudaError_t launch_plan_whole(long long n, Ctl *ctl, int log2c, int tile_keys, c
 template <typename K>
 cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void *S, void *samp, long long max_tiles,
                                cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg, const void *src_split,
-                               const uint32_t *cflag) {
+                               const uint32_t *cflag, const void *src_pad) {
     using G = SGeo<K>;
     constexpr size_t smem = TSGeo<K, G::kNT, G::kVT>::bytes();
     auto kern = k_tile_sort<K, G::kNT, G::kVT, G::kMinB, G::kBuckets, G::kCap>;
     if (max_tiles <= 0) return cudaSuccess;
     prof_begin(kProfTileSort, st);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)max_tiles), dim3(G::kNT), smem, st, plan, (const K *)src, (K *)F,
-                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F), cflag);
+                               (K *)S, (K *)samp, sbtab, scfg, (const K *)(src_split ? src_split : F), cflag,
+                               (const K *)src_pad);
     if (e != cudaSuccess) return e;
     prof_end(kProfTileSort, st);
     return cudaGetLastError();
@@ -777,9 +780,11 @@ cudaError_t launch_tile_sort_t(const Plan *plan, const void *src, void *F, void 
 
 cudaError_t launch_tile_sort(int dt, const Plan *plan, const void *src, void *F, void *S, void *samp,
                              long long max_tiles, cudaStream_t st, const uint32_t *sbtab, const SplitCfg *scfg,
-                             const void *src_split, const uint32_t *cflag) {
-    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag)
-                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag);
+                             const void *src_split, const uint32_t *cflag, const void *src_pad) {
+    return dt == 0 ? launch_tile_sort_t<int32_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag,
+                                                 src_pad)
+                   : launch_tile_sort_t<int64_t>(plan, src, F, S, samp, max_tiles, st, sbtab, scfg, src_split, cflag,
+                                                 src_pad);
 }
 
 }  // namespace hs

@@ -390,3 +390,40 @@ def test_split_constant_piece_in_a_bucket_that_falls_back():
     keys = np.concatenate([chunk0, chunk1, rest]).astype(np.int32)   # bucket 3 in this order: chunk 0 then 1
     plan = check(keys, D, c)
     assert plan["split"][3] == 0, plan
+
+
+def _hidden_cluster(n, D, dtype, seed):
+    """One bucket, one chunk (c = 1): every position K5a's phase-1 sample reads
+    ((r n) >> 15 for r = 0, 8, ..., 32760; k_split_sample_map) holds a uniform key of
+    digit 1, every other position a key of one narrow value range -- the sample sees a
+    uniform bucket, so the bucket takes the padded layout (no count pass), and one
+    region overflows: k_split_pad_plan must send the bucket back to the leaf plan."""
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(seed)
+    keys = (div + div // 2 + rng.integers(0, 1000, n)).astype(dtype)   # the hidden cluster
+    pos = (np.arange(0, 1 << 15, 8, dtype=np.int64) * n) >> 15
+    keys[pos] = (div + rng.integers(0, div, pos.size)).astype(dtype)
+    return keys
+
+
+@pytest.mark.parametrize("dtype,D", [(np.int32, 9), (np.int64, 18)])
+def test_split_padded_region_overflow_falls_back(dtype, D):
+    n = 1 << 20
+    keys = _hidden_cluster(n, D, dtype, 77)
+    plan = check(keys, D, 1)
+    assert plan["split"][1] == 0, plan          # the overflow was caught after the scatter
+
+
+@pytest.mark.parametrize("dtype,D", [(np.int32, 9), (np.int64, 18)])
+def test_split_padded_next_to_counted_buckets(dtype, D):
+    """Padded (uniform) buckets beside a counted one (a dense core: constant tracking, sampled
+    map) and a bucket whose padded region overflows -- each path in one call."""
+    t, c = T(0 if dtype == np.int32 else 1), 4
+    div = 10 ** (D - 1)
+    rng = np.random.default_rng(5)
+    uni = buckets([c * 3 * t] * 10, D, 61, dtype=dtype)
+    core = (5 * div + rng.integers(0, 1000, c * 3 * t)).astype(dtype)   # bucket 5: dense core
+    hid = _hidden_cluster(c * 6 * t, D, dtype, 62)                       # bucket 1: hidden cluster
+    keys = np.concatenate([uni, core, hid])
+    plan = check(keys, D, c)
+    assert sum(plan["split"][b] for b in (0, 2, 3, 4, 6, 7, 8, 9)) == 8, plan
