@@ -347,9 +347,12 @@ def run_ours(args, cfg):
     L_launch = per_kernel.get("merge_level", {}).get("launches_per_step", 0)
     level_bytes = [2 * ksize * int(sum(m[b] for b in range(10) if levels[b] > lv)) for lv in range(L_launch)]
     m_split = int(sum(m[b] for b in range(10) if split[b]))
+    # the count pass reads only the split buckets that are not in the padded layout
+    padded = dplan.get("padded", [0] * 10) if (not shared and not pairs) else [0] * 10
+    m_count = int(sum(m[b] for b in range(10) if split[b] and not padded[b]))
     alg = {  # algorithmic bytes per step of each kernel kind
         "tile_hist": ksize * cfg.n, "scatter": 2 * ksize * cfg.n, "tile_sort": 2 * ksize * cfg.n,
-        "merge_level": sum(level_bytes), "split_count": ksize * m_split, "split_scatter": 2 * ksize * m_split,
+        "merge_level": sum(level_bytes), "split_count": ksize * m_count, "split_scatter": 2 * ksize * m_split,
     }
     if pairs:  # K0 + K8: pack (r 4 + w 8) and unpack (r 8, tag gather 8, w 4 + 8); KV: r 8 + 8, w 16 and back
         alg["copy"] = cfg.n * (64 if kv else 40)
@@ -370,7 +373,7 @@ def run_ours(args, cfg):
                 "launches_per_step": per_kernel[dom]["launches_per_step"],
                 "active_launches_per_step": len(active) if dom == "merge_level" else 1}
     # hist r + scatter r/w (MSD path only) + K5a split count r + scatter r/w (split buckets) + tile sort r/w + merge levels
-    path_bytes = ksize * cfg.n * (2 if shared else 5) + 3 * ksize * m_split + sum(level_bytes)
+    path_bytes = ksize * cfg.n * (2 if shared else 5) + ksize * m_count + 2 * ksize * m_split + sum(level_bytes)
     if pairs and not kv:  # pack (r 4 + w 8), tag copy (r 8 + w 8), unpack (r 8 + tag gather 8 + w 4 + w 8)
         path_bytes += cfg.n * (12 + 16 + 28)
     elif kv:  # pack (r 8 + 8, w 16), unpack (r 16, w 8 + 8)

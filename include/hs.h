@@ -337,9 +337,11 @@ hs_status_t hs_sort_buckets(void *keys, int64_t n, hs_dtype_t dtype, int num_dig
  * K5a value split takes, hence how many merge levels run).  Runs the
  * partition and the split into scratch memory (keys is not modified),
  * synchronises the stream and writes, per bucket b (host arrays of 10):
- * levels_out[b] = merge levels L[b], split_out[b] = 1 if bucket b's chunks
- * were value-split, leaves_out[b] = tile-sort leaves per chunk.  Arguments
- * and errors as hs_sort.
+ * levels_out[b] = merge levels L[b], split_out[b] = 0 if bucket b's chunks
+ * were not value-split, 1 if they were (sub-ranges counted by the K5a count
+ * pass), 2 if they were in the padded layout (no count pass: one tile-sized
+ * region per chunk sub-range), leaves_out[b] = tile-sort leaves per chunk.
+ * Arguments and errors as hs_sort.
  */
 hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int chunks_per_bucket,
                          int32_t *levels_out, int32_t *split_out, int32_t *leaves_out, cudaStream_t stream);

@@ -300,7 +300,8 @@ def hs_sort_buckets(keys, bucket_offsets, num_digits: int, chunks_per_bucket: in
 
 def hs_sort_plan(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None):
     """The plan hs_sort would run on keys (keys unchanged): dict of per-bucket
-    merge levels, K5a split flags and tile-sort leaves per chunk."""
+    merge levels, K5a split flags (and whether the split used the padded
+    layout) and tile-sort leaves per chunk."""
     import numpy as np
     torch = _torch()
     _check_tensor(keys, "keys")
@@ -311,7 +312,8 @@ def hs_sort_plan(keys, num_digits: int, chunks_per_bucket: int = 8, stream=None)
     with torch.cuda.device(keys.device):
         _check(load().hs_sort_plan(keys.data_ptr(), keys.numel(), dt, num_digits, chunks_per_bucket,
                                    L.ctypes.data, sp.ctypes.data, lv.ctypes.data, _stream(stream)))
-    return {"levels": L.tolist(), "split": sp.tolist(), "leaves": lv.tolist()}
+    return {"levels": L.tolist(), "split": [int(v != 0) for v in sp.tolist()],
+            "padded": [int(v == 2) for v in sp.tolist()], "leaves": lv.tolist()}
 
 
 def hs_sort_shared(keys, chunks: int = 8, stream=None):

@@ -466,12 +466,67 @@ hs_status_t hs_msd_partition(const void *keys, int64_t n, hs_dtype_t dtype, int 
 
 namespace {
 
+// CUDA-graph capture: the side stream a conditional node's body is captured on
+// (one per host thread and device, created by an uncaptured call -- creating a
+// stream inside a global-mode capture is not allowed), or null when `stream` is
+// not capturing / no side stream exists yet (the caller then launches directly).
+cudaStream_t capture_side_stream(cudaStream_t stream) {
+    static thread_local cudaStream_t side[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (cs == cudaStreamCaptureStatusNone) {
+        if (!side[dev] && cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            side[dev] = nullptr;
+        }
+        return nullptr;
+    }
+    return cs == cudaStreamCaptureStatusActive ? side[dev] : nullptr;
+}
+
+// In the graph `stream` is capturing: a k_level_gate node (plan Lmax > lv), then an IF node whose
+// body -- captured on `side` by body(side) -- runs only when the gate opened it.
+template <typename Body>
+cudaError_t gated_levels(cudaStream_t stream, cudaStream_t side, const hs::Plan *plan, int lv, Body body) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
+    if ((e = hs::launch_level_gate((unsigned long long)h, plan, lv, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamGetCaptureInfo(stream, &cs, nullptr, &g, &deps, &nd)) != cudaSuccess) return e;
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((e = cudaGraphAddNode(&node, g, deps, nd, &p)) != cudaSuccess) return e;
+    if ((e = cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+        return e;
+    if ((e = cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+        return e;
+    const cudaError_t eb = body(side);
+    cudaGraph_t out = nullptr;
+    e = cudaStreamEndCapture(side, &out);
+    return eb != cudaSuccess ? eb : e;
+}
+
 // a1-a7 on validated arguments (n > 0).  key_shift as partition_impl.
 // user_off (device int64[11], hs_sort_buckets): keys are already partitioned by
 // digit into those buckets -- a1-a3 are skipped, the plan comes from user_off,
 // the split reads keys and writes the scratch, the tile sort reads both.
 hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, int key_shift, int chunks_per_bucket,
-                      int log2c, cudaStream_t stream, hs::Plan *inspect = nullptr,
+                      int log2c, cudaStream_t stream, hs::Ctl *inspect = nullptr,
                       const int64_t *user_off = nullptr) {
     hs_status_t s;
     int sms;
@@ -506,7 +561,7 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
         if (e2 == cudaSuccess && split_on)
             e2 = hs::launch_split(dt, ws.ctl, ws.S, F, ws.sbtab, ws.sbcur, split_words, n, log2c, T, div, key_shift,
                                   F, ws.pad, pad_keys, stream);
-        if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, &ws.ctl->plan, sizeof(hs::Plan), cudaMemcpyDeviceToHost, stream);
+        if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(inspect, ws.ctl, sizeof(hs::Ctl), cudaMemcpyDeviceToHost, stream);
         cudaError_t fe = cudaFreeAsync(ws.base, stream);
         if (e2 == cudaSuccess) e2 = fe;
         if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(stream);
@@ -541,12 +596,32 @@ hs_status_t sort_impl(void *keys, int64_t n, hs_dtype_t dtype, int num_digits, i
                                      ws.sbtab, &ws.ctl->split, spl,
                                      split_on ? hs::split_cflag(ws.sbcur, split_words) : nullptr, ws.pad),
                 "K5 tile sort");
-    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys
+    // a5 (in-chunk levels) + a6 (tree merge of chunks): ping-pong, last level lands in keys.
+    // Every plan runs the log2 c tree levels (L[b] = k[b] + log2 c); the host only knows a bound on
+    // the rest (fallback buckets' in-chunk levels).  Under CUDA-graph capture those sit behind a
+    // conditional node the device plan opens (k_level_gate); otherwise they are launched and exit
+    // at once when the plan has no bucket there.
     const int L = level_bound(n, log2c, T, 1, 1);
-    for (int lv = 0; lv < L; ++lv) {
-        HS_TRY_CUDA(hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
-                                           lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, stream),
-                    "K6 merge level");
+    const int Lsure = L < log2c ? L : log2c;
+    auto level = [&](int lv, cudaStream_t st) {
+        return hs::launch_merge_level(dt, plan, keys, ws.S, nullptr, ws.corank, ws.samp[lv & 1],
+                                      lv + 1 < L ? ws.samp[(lv + 1) & 1] : nullptr, lv, (int)n, sms, st);
+    };
+    for (int lv = 0; lv < Lsure; ++lv) HS_TRY_CUDA(level(lv, stream), "K6 merge level");
+    if (L > Lsure) {
+        cudaStream_t side = capture_side_stream(stream);
+        if (side) {
+            HS_TRY_CUDA(gated_levels(stream, side, plan, Lsure, [&](cudaStream_t st) -> cudaError_t {
+                            for (int lv = Lsure; lv < L; ++lv) {
+                                const cudaError_t e = level(lv, st);
+                                if (e != cudaSuccess) return e;
+                            }
+                            return cudaSuccess;
+                        }),
+                        "K6 gated merge levels");
+        } else {
+            for (int lv = Lsure; lv < L; ++lv) HS_TRY_CUDA(level(lv, stream), "K6 merge level");
+        }
     }
     cudaError_t fe = cudaFreeAsync(ws.base, stream);
     if (fe != cudaSuccess) return cuda_fail(fe, "cudaFreeAsync");
@@ -610,17 +685,18 @@ hs_status_t hs_sort_plan(const void *keys, int64_t n, hs_dtype_t dtype, int num_
     if ((s = check_chunks(chunks_per_bucket, &log2c)) != HS_OK) return s;
     if ((s = check_ptr(keys, n, dtype, "keys")) != HS_OK) return s;
     if (!levels_out || !split_out || !leaves_out) return fail(HS_ERR_INVALID_VALUE, "output array is NULL");
-    hs::Plan P;
-    memset(&P, 0, sizeof(P));
+    hs::Ctl X;
+    memset(&X, 0, sizeof(X));
+    const hs::Plan &P = X.plan;
     if (n > 0) {
         g_launch_counter = 0;
-        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &P)) !=
+        if ((s = sort_impl(const_cast<void *>(keys), n, dtype, num_digits, 0, chunks_per_bucket, log2c, stream, &X)) !=
             HS_OK)
             return s;
     }
     for (int b = 0; b < 10; ++b) {
         levels_out[b] = n > 0 ? P.L[b] : 0;
-        split_out[b] = P.split[b];
+        split_out[b] = P.split[b] ? (hs::split_pmode(X.split, b) ? 2 : 1) : 0;
         leaves_out[b] = P.split[b] ? P.nsb[b] : (1 << P.k[b]);
     }
     g_launches = 0;

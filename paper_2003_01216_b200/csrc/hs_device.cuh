@@ -200,7 +200,7 @@ struct SplitCfg {
 
 // Padded layout for bucket b: room in the pad buffer, equal-width sub-ranges (the
 // sample found no skew) and no constant tracking.
-__device__ __forceinline__ bool split_pmode(const SplitCfg &C, int b) {
+__host__ __device__ __forceinline__ bool split_pmode(const SplitCfg &C, int b) {
     return C.pad[b] && !C.mode[b] && !C.cc[b];
 }
 

@@ -70,6 +70,8 @@ cudaError_t launch_split(int dt, Ctl *ctl, const void *S, void *F, uint32_t *tab
 // the samples this level writes for the next one (may be null).
 cudaError_t launch_merge_level(int dt, const Plan *plan, void *F, void *S, const void *src0, int *corank,
                                const void *samp_in, void *samp_out, int level, int n, int num_sms, cudaStream_t st);
+// One-thread kernel: sets the conditional graph node handle to (plan Lmax > lv).
+cudaError_t launch_level_gate(unsigned long long handle, const Plan *plan, int lv, cudaStream_t st);
 // samp[m] = src[m*kSampleQ + kSampleQ-1] (hs_merge: samples of the caller's runs)
 cudaError_t launch_sample(int dt, const void *src, void *samp, long long n, int num_sms, cudaStream_t st);
 cudaError_t launch_copy(int dt, const void *src, void *dst, long long n, int num_sms, cudaStream_t st);

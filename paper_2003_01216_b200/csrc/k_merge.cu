@@ -408,6 +408,21 @@ __global__ void __launch_bounds__(NC + 32) k_merge_level(const Plan *__restrict_
     if (tid == 0) bulk_wait0();
 }
 
+// ============================================================ level gate
+// CUDA-graph capture of hs_sort: the merge levels the host launches past the
+// log2 c tree levels every plan runs (k[b] + log2 c >= log2 c) sit in the body
+// of a conditional (IF) graph node; this one-thread kernel opens it only when
+// the device plan has a bucket with more levels (a fallback bucket), so a
+// replay of a C3 sort skips all the empty level launches.
+__global__ void k_level_gate(cudaGraphConditionalHandle h, const Plan *__restrict__ plan, int lv) {
+    griddep_wait();
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, plan->Lmax > lv ? 1u : 0u);
+}
+
+cudaError_t launch_level_gate(unsigned long long handle, const Plan *plan, int lv, cudaStream_t st) {
+    return launch_pdl(k_level_gate, dim3(1), dim3(32), 0, st, (cudaGraphConditionalHandle)handle, plan, lv);
+}
+
 // =================================================================== K7
 template <typename K>
 __global__ void k_copy(const K *__restrict__ src, K *__restrict__ dst, long long n) {

@@ -73,6 +73,7 @@ def test_split_uniform_all_buckets(c):
     plan = check(keys, 9, c)
     lg = c.bit_length() - 1
     assert plan["split"] == [1] * 10
+    assert plan["padded"] == [1] * 10           # uniform buckets: padded layout, no count pass
     assert plan["levels"] == [lg] * 10          # only the paper's chunk tree remains
     assert all(lv >= 2 for lv in plan["leaves"])
 
@@ -427,3 +428,32 @@ def test_split_padded_next_to_counted_buckets(dtype, D):
     keys = np.concatenate([uni, core, hid])
     plan = check(keys, D, c)
     assert sum(plan["split"][b] for b in (0, 2, 3, 4, 6, 7, 8, 9)) == 8, plan
+    assert sum(plan["padded"][b] for b in (0, 2, 3, 4, 6, 7, 8, 9)) == 8, plan
+    assert plan["padded"][5] == 0, plan         # the dense core is counted (constant tracking)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "fallback"])
+def test_graph_replay_gates_extra_levels(kind):
+    """SortGraph (CUDA-graph capture of hs_sort): the merge levels past the log2 c tree levels sit
+    behind a conditional node the device plan opens.  A uniform input skips them; a padded bucket
+    that overflows (fallback: k in-chunk levels) needs them -- both must replay to the oracle's
+    result, twice (the gate is re-evaluated on every replay)."""
+    t = T(0)
+    if kind == "uniform":
+        keys = buckets([2 * 3 * t] * 10, 9, 71)
+        c = 2
+    else:
+        keys = _hidden_cluster(1 << 20, 9, np.int32, 72)
+        c = 1
+    d = torch.from_numpy(np.ascontiguousarray(keys)).to(DEV)
+    plan = hs.hs_sort_plan(d, 9, c)
+    if kind == "fallback":
+        assert plan["split"][1] == 0 and plan["levels"][1] > 0, plan
+    buf = torch.empty_like(d)
+    g = hs.SortGraph(buf, 9, c)
+    ref = O.sort(keys, 9, c)
+    for _ in range(2):
+        buf.copy_(d)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy(), ref)
