@@ -22,6 +22,8 @@ ap.add_argument("--n", type=int, required=True)
 ap.add_argument("--ksize", type=int, required=True)
 ap.add_argument("--last-call", action="store_true")
 ap.add_argument("--levels", type=int, default=3, help="active merge levels per step (for the alg. bytes)")
+ap.add_argument("--counted", type=float, default=0.0,
+                help="share of the keys in counted (not padded) split buckets: the count pass reads only those")
 args = ap.parse_args()
 
 rows = list(csv.DictReader(l for l in open(args.csv) if not l.startswith("==")))
@@ -43,7 +45,7 @@ def v(m, k):
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 nb = args.n * args.ksize
-ALG = {"k_tile_hist": nb, "k_scatter": 2 * nb, "k_split_count": nb, "k_split_scatter": 2 * nb, "k_tile_sort": 2 * nb,
+ALG = {"k_tile_hist": nb, "k_scatter": 2 * nb, "k_split_count": nb * args.counted, "k_split_scatter": 2 * nb, "k_tile_sort": 2 * nb,
        "k_merge_level": 2 * nb, "k_tree_merge": 2 * nb}
 agg = collections.OrderedDict()
 for (i, name), m in items:
