@@ -432,6 +432,22 @@ __device__ __forceinline__ int sub_range_of(int64_t k, int shift, long long lo, 
     return (int)min((long long)__umul64hi((unsigned long long)d, mul), (long long)(ns - 1));
 }
 
+// Ranks in duplicate-heavy slices (buckets with constant tracking: one value may fill a
+// whole slice, and 32 lanes taking ranks from one shared counter serialise): a warp whose
+// 32 keys all fall in one sub-range takes 32 ranks at once.  All 32 lanes call it (slots
+// past a slice's end carry the dummy sub-range).  (The count pass measured slower with
+// the same test: its plain atomics return nothing.)
+__device__ __forceinline__ uint32_t warp_rank(uint32_t *hist, int t) {
+    const int lane = threadIdx.x & 31;
+    const int t0 = __shfl_sync(0xffffffffu, t, 0);
+    if (__all_sync(0xffffffffu, t == t0)) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&hist[t0], 32u);
+        return __shfl_sync(0xffffffffu, base, 0) + (uint32_t)lane;
+    }
+    return atomicAdd(&hist[t], 1u);
+}
+
 // In-place exclusive scan of a[0, n) by the whole CTA (NT threads, contiguous
 // segments per thread).  Ends with a barrier.
 template <int NT>
@@ -568,14 +584,16 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
                 const long long lo = d.lo;
                 const unsigned long long mul = d.mul;
 #pragma unroll
-                for (int k = 0; k < VT; ++k)
-                    atomicAdd(&hist[k * NT + tid < cnt ? sub_range_of(v[k], d.shift, lo, mul, ns) : ns], 1u);
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NT + tid < cnt ? sub_range_of(v[k], d.shift, lo, mul, ns) : ns;
+                    atomicAdd(&hist[t], 1u);
+                }
             } else {
 #pragma unroll
-                for (int k = 0; k < VT; ++k)
-                    atomicAdd(&hist[k * NT + tid < cnt ? (int)__ldg(d.bmap + fine_bin<K>(v[k], d.shift, d.lo, d.fmul))
-                                                       : ns],
-                              1u);
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NT + tid < cnt ? (int)__ldg(d.bmap + fine_bin<K>(v[k], d.shift, d.lo, d.fmul)) : ns;
+                    atomicAdd(&hist[t], 1u);
+                }
             }
             if (cc) {
 #pragma unroll 4
@@ -626,12 +644,19 @@ __global__ void __launch_bounds__(NT, MINB) k_split_count(const Ctl *__restrict_
 // at their slice-local sorted position, then written in staged order with
 // their sub-range recomputed: consecutive threads write consecutive addresses
 // inside a sub-range.
-template <typename K, int NT, int VT, int MINB>
+// CC = false: the slices of buckets without constant tracking (the usual case); CC = true: only
+// those of C.cc buckets, ranked with warp_rank (exits at once when there are none).
+template <typename K, int NT, int VT, int MINB, bool CC>
 __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restrict__ ctl, const K *__restrict__ S,
                                                             K *__restrict__ F, uint32_t *cur, int nsb_cap,
                                                             const uint16_t *map, K *__restrict__ padbuf,
                                                             int cap_keys) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
+    if (CC) {
+        bool any = false;
+        for (int b = 0; b < 10; ++b) any |= ctl->split.cc[b] != 0 && ctl->plan.split[b] != 0;
+        if (!any) return;
+    }
     constexpr int TS = NT * VT;
     static_assert(TS <= 65536, "ranks are packed in 16 bits");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -648,10 +673,12 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     long long g = blockIdx.x;
     if (tid == 0) slice_desc(sd[0], ctl, g, true, TS, map);
     __syncthreads();
+    // this instantiation's slices only (a skipped slice's descriptor has cnt = 0 or another cc)
+    auto mine = [](const SliceDesc &x) -> int { return (x.cnt > 0 && (x.cc != 0) == CC) ? x.cnt : 0; };
     K v[VT];
     {
         const K *in = S + sd[0].cs + sd[0].a0;
-        const int cnt = sd[0].cnt;
+        const int cnt = mine(sd[0]);
 #pragma unroll
         for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cnt ? in[k * NT + tid] : K(0);
     }
@@ -660,13 +687,14 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
     for (; g < nslices; g += gridDim.x, cb ^= 1) {
         const SliceDesc &d = sd[cb];
         if (tid == 0) slice_desc(sd[cb ^ 1], ctl, g + gridDim.x, true, TS, map);
-        const int cnt = d.cnt, ns = d.ns;
-        if (cnt == 0) {  // nothing here (fallback bucket / past the chunk's end): load the next slice
+        const int cnt = mine(d), ns = d.ns;
+        if (cnt == 0) {  // nothing here (fallback bucket / past the chunk's end / other instantiation)
             __syncthreads();
             const SliceDesc &dn = sd[cb ^ 1];
             const K *in = S + dn.cs + dn.a0;
+            const int cn = mine(dn);
 #pragma unroll
-            for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < dn.cnt ? in[k * NT + tid] : K(0);
+            for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cn ? in[k * NT + tid] : K(0);
             __syncthreads();
             continue;
         }
@@ -681,13 +709,13 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
 #pragma unroll
                 for (int k = 0; k < VT; ++k) {
                     const int t = k * NT + tid < cnt ? sub_range_of(v[k], shift, lo, mul, ns) : ns;
-                    tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+                    tr[k] = ((uint32_t)t << 16) | (CC ? warp_rank(hist, t) : atomicAdd(&hist[t], 1u));
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < VT; ++k) {
                     const int t = k * NT + tid < cnt ? (int)__ldg(bmap + fine_bin<K>(v[k], shift, lo, fmul)) : ns;
-                    tr[k] = ((uint32_t)t << 16) | atomicAdd(&hist[t], 1u);
+                    tr[k] = ((uint32_t)t << 16) | (CC ? warp_rank(hist, t) : atomicAdd(&hist[t], 1u));
                 }
             }
         }
@@ -718,7 +746,7 @@ __global__ void __launch_bounds__(NT, MINB) k_split_scatter(const Ctl *__restric
         const SliceDesc &dn = sd[cb ^ 1];
         {
             const K *in = S + dn.cs + dn.a0;
-            const int cn = dn.cnt;
+            const int cn = mine(dn);
 #pragma unroll
             for (int k = 0; k < VT; ++k) v[k] = k * NT + tid < cn ? in[k * NT + tid] : K(0);
             const int nz = (cn > 0 && dn.ns > ns) ? dn.ns : ns;
@@ -970,7 +998,10 @@ cudaError_t setup_split_t() {
     e = cudaFuncSetAttribute(k_split_count<K, G::NT, G::VT, G::MINB_COUNT, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_count);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>,
+    e = cudaFuncSetAttribute(k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_scat);
 }
 
@@ -1018,7 +1049,8 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
         (((size_t)(nsb_cap + 1) * 4 + 15) & ~(size_t)15) + (size_t)(nsb_cap + 1) * 8 + (size_t)TS * sizeof(K);
     auto kc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, false>;
     auto kcc = k_split_count<K, G::NT, G::VT, G::MINB_COUNT, true>;
-    auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT>;
+    auto ks = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT, false>;
+    auto ksc = k_split_scatter<K, G::NT, G::VT, G::MINB_SCAT, true>;
     cudaError_t e;
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
@@ -1058,6 +1090,9 @@ static cudaError_t launch_split_t(Ctl *ctl, const K *S, K *F, uint32_t *tab, uin
     prof_begin(kProfSplitScatter, st);
     const long long sgrid = grid < (long long)sms * G::MINB_SCAT ? grid : (long long)sms * G::MINB_SCAT;
     if ((e = launch_pdl(ks, dim3((unsigned)sgrid), dim3(G::NT), sm_scat, st, ctl, S, F, cur, nsb_cap, map, padbuf,
+                        tile_keys)) != cudaSuccess)
+        return e;
+    if ((e = launch_pdl(ksc, dim3((unsigned)sgrid), dim3(G::NT), sm_scat, st, ctl, S, F, cur, nsb_cap, map, padbuf,
                         tile_keys)) != cudaSuccess)
         return e;
     HS_SPLIT_STEP(5);
