@@ -22,10 +22,17 @@
  *    enqueue kernels on `stream` (NULL = the legacy default stream) of the
  *    current device, and return.  No call synchronises the host, so a whole
  *    call can be captured in a CUDA graph.  Scratch (one n-key ping-pong
- *    buffer, lookback status words, plan and co-rank tables) is taken with
- *    stream-ordered cudaMallocAsync/cudaFreeAsync from the device's default
- *    memory pool, whose release threshold the library raises so repeated
- *    calls do not remap memory.
+ *    buffer, lookback status words, plan and co-rank tables, and for
+ *    hs_sort / hs_sort_buckets / hs_sort_pairs on chunks larger than one
+ *    tile the K5a split table plus the padded-layout buffer of about
+ *    1.11 n + 10 c T keys) is taken with stream-ordered
+ *    cudaMallocAsync/cudaFreeAsync from the device's default memory pool,
+ *    whose release threshold the library raises so repeated calls do not
+ *    remap memory.  Under CUDA-graph capture, hs_sort puts the merge levels
+ *    past the log2 c tree rounds behind a conditional graph node that the
+ *    device plan opens (their body is captured on a per-thread side stream
+ *    the first uncaptured call on that thread creates; without one they
+ *    are captured as plain launches).
  *  - Calls are reentrant and may run concurrently on distinct streams over
  *    distinct buffers.
  *  - Validation happens before any launch; on an error nothing is enqueued and
