@@ -32,7 +32,26 @@ for name in names:
                 ts.append(s.elapsed_time(e))
         res[what] = float(np.median(ts))
     ok = bool(torch.all(buf[1:] >= buf[:-1]))
+    launches = hs.last_launch_count()
+    # the same call replayed from a CUDA graph (SortGraph; the bench's launch configuration): no
+    # per-launch host work, the merge levels past the tree rounds behind the device-opened gate
+    gbuf = src.clone()
+    g = hs.SortGraph(gbuf, cfg.num_digits, cfg.chunks)
+    ts = []
+    for it in range(8):
+        gbuf.copy_(src)
+        torch.cuda.synchronize()
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        if it >= 3:
+            ts.append(s.elapsed_time(e))
+    res["graph"] = float(np.median(ts))
+    ok = ok and bool(torch.all(gbuf[1:] >= gbuf[:-1]))
     print(f"{name}: n={cfg.n} partition {res['partition']:.3f} ms  sort {res['sort']:.3f} ms "
-          f"= {cfg.n / res['sort'] / 1e6:.2f} Gkeys/s  sorted={ok} launches={hs.last_launch_count()}", flush=True)
+          f"= {cfg.n / res['sort'] / 1e6:.2f} Gkeys/s  graph {res['graph']:.3f} ms = "
+          f"{cfg.n / res['graph'] / 1e6:.2f} Gkeys/s  sorted={ok} launches={launches}", flush=True)
+    del g, gbuf
     del src, buf, out
     torch.cuda.empty_cache()
