@@ -25,5 +25,5 @@ done
 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/b_short.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file $OUT/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 python tools/one_call.py C3 sort 2 > $OUT/one.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_tile_hist|k_scatter|k_split_count|k_split_scatter|k_tile_sort|k_merge_level|k_merge_partition" -s 34 -c 8 -o $OUT/full python tools/one_call.py C3 sort 2 > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_tile_hist|k_scatter|k_split_count|k_split_scatter|k_tile_sort|k_merge_level|k_merge_partition" -s 35 -c 9 -o $OUT/full python tools/one_call.py C3 sort 2 > $OUT/ncu_full.log 2>&1
 ls -la $OUT
