@@ -81,6 +81,9 @@ struct SplGeo<int64_t> {
 constexpr int kSplitMaxSub = 4096;  // sub-ranges per chunk (shared-memory counters)
 constexpr int kSplitPlanNT = 512;
 
+#ifndef HS_SPLIT_MAP_PCT
+#define HS_SPLIT_MAP_PCT 70  // sampled-map sub-ranges: this share of a tile (slack for the sampling error)
+#endif
 #ifndef HS_SPLIT_TARGET_PCT
 #define HS_SPLIT_TARGET_PCT 90
 #endif
@@ -93,7 +96,7 @@ __host__ __device__ __forceinline__ long long split_target(int tile_keys) {
 // ------------------------------------------------------------------ setup
 // Row capacity per chunk for a sampled (skewed) bucket: sub-ranges of ~0.7 T
 // keys (slack for the sampling error of the map).
-__host__ __device__ __forceinline__ long long split_target_map(int tile_keys) { return (long long)tile_keys * 7 / 10; }
+__host__ __device__ __forceinline__ long long split_target_map(int tile_keys) { return (long long)tile_keys * HS_SPLIT_MAP_PCT / 100; }
 
 // Constant over-full sub-ranges (a value with more copies in a chunk than the
 // big-piece path takes, e.g. all keys equal): for buckets whose sample shows a

@@ -6,6 +6,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2003_01216_b200 as hs
 
+if os.environ.get("HS_VARIANT"):  # a variant build from tools/exp.py (var/NAME/libhybridsort.so)
+    hs._LIB = hs.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "var",
+                                   os.environ["HS_VARIANT"], "libhybridsort.so"))
+
 n = 1 << 28
 g = torch.Generator(device="cuda").manual_seed(7)
 def uni(lo, hi, size):
