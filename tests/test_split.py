@@ -457,3 +457,25 @@ def test_graph_replay_gates_extra_levels(kind):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(buf.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("power", [4, 12])
+def test_tile_rebucket_steep_density(power):
+    """Leaves whose keys crowd one end of their range (density ~ x^(1/p - 1)): the tile sort's
+    equal-width buckets overflow there, and the tile re-buckets by an equal-count map interpolated
+    from its first-pass histogram (or, if that still overflows, takes the merge rounds) -- bit-exact
+    either way, through hs_sort (chunks of one tile: no split) and hs_sort_chunks."""
+    t, c = T(0), 8
+    rng = np.random.default_rng(90 + power)
+    n = c * (t - 1000)
+    u = rng.random(n)
+    keys = (10**8 + np.floor(u ** power * (10**8 - 1))).astype(np.int32)
+    check(keys, 9, c)
+    d = torch.from_numpy(keys).to(DEV)
+    out, off = hs.hs_msd_partition(d, 9)
+    chunks = torch.empty_like(out)
+    hs.hs_sort_chunks(out, off, c, out=chunks)
+    torch.cuda.synchronize()
+    p_ref, off_ref = O.msd_partition(keys, 9)
+    ref = O.sort_chunks(p_ref, off_ref, c)
+    assert np.array_equal(chunks.cpu().numpy(), ref)
