@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tile_sort(const Plan *__restrict__
                                                         const uint32_t *__restrict__ cflag, const K *src_pad) {
     griddep_wait();  // PDL: the predecessor kernel's writes are visible from here
     static_assert(VT & 1, "odd VT keeps blocked shared-memory accesses conflict-free");
+    // the grid is a host bound on the leaves: CTAs past the device plan's count leave before any setup
+    if ((long long)blockIdx.x >= __ldg(&plan_g->tile_prefix[10])) return;
     using G = TSGeo<K, NT, VT>;
     constexpr int T = G::T, E = G::E;
     extern __shared__ __align__(128) unsigned char smem_raw[];
