@@ -46,7 +46,7 @@ peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 nb = args.n * args.ksize
 ALG = {"k_tile_hist": nb, "k_scatter": 2 * nb, "k_split_count": nb * args.counted, "k_split_scatter": 2 * nb, "k_tile_sort": 2 * nb,
-       "k_merge_level": 2 * nb, "k_tree_merge": 2 * nb}
+       "k_merge_level": 2 * nb}
 agg = collections.OrderedDict()
 for (i, name), m in items:
     short = name.split("(")[0].replace("void ", "").replace("hs::", "").split("<")[0]

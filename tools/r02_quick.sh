@@ -2,7 +2,7 @@
 set -x
 OUT=${1:-gpurun_out/r02q}
 mkdir -p $OUT
-timeout 900 python -m pytest tests/test_tree.py tests/test_split.py tests/test_shapes.py -x -q > $OUT/tests.log 2>&1
+timeout 900 python -m pytest tests/test_split.py tests/test_shapes.py -x -q > $OUT/tests.log 2>&1
 tail -3 $OUT/tests.log
 python bench.py --no-cpu-baseline > $OUT/bench_C3.json 2> $OUT/bench_C3.log
 grep "\[bench\]" $OUT/bench_C3.log
