@@ -1,4 +1,4 @@
-"""Per-kernel table from an ncu --csv --metrics launch list (tools/r02_call.sh):
+"""Per-kernel table from an ncu --csv --metrics launch list (tools/r02_full.sh):
 duration, DRAM read/write bytes, GB/s, fraction of the measured HBM peak, algorithmic
 bytes (a read and a write of the keys a pass moves; given per kernel
 on the command line), and shared-memory bank-conflict wavefronts next to total
