@@ -3,7 +3,7 @@ on the GPU -- every 32-bit position, cursor and leaf index at its limit (split t
 regions, merge blocks).  The oracle would take minutes at this size, so the result is checked by
 properties that hold at any size: non-decreasing order, and the same multiset as the input
 (count, sum, sum of squares and a 65,536-bin histogram of the low 16 bits), computed with
-torch in slices on the device.  D = 9 runs the K5a split (padded layout) everywhere; D = 10 over
+torch in slices on the device; int64 keys (D = 18) as well.  D = 9 runs the K5a split (padded layout) everywhere; D = 10 over
 [0, 2^31 - 1) fills only buckets 0-2, whose chunks (~125M keys) need more sub-ranges than the split
 takes (4096), so they run the leaf plan: 13 in-chunk merge levels + the 3 tree levels."""
 import pytest
@@ -35,15 +35,17 @@ def _sorted(x):
     return ok
 
 
-@pytest.mark.parametrize("D,hi", [(9, 10**9), (10, 2**31 - 1)])
-def test_max_size_hs_sort(D, hi):
+@pytest.mark.parametrize("dtype,D,hi", [(torch.int32, 9, 10**9), (torch.int32, 10, 2**31 - 1),
+                                        (torch.int64, 18, 10**18)])
+def test_max_size_hs_sort(dtype, D, hi):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     free, _ = torch.cuda.mem_get_info()
-    if free < 40 * (1 << 30):
-        pytest.skip("needs ~40 GiB of free device memory")
+    need = (40 if dtype == torch.int32 else 80) * (1 << 30)
+    if free < need:
+        pytest.skip(f"needs ~{need >> 30} GiB of free device memory")
     g = torch.Generator(device="cuda").manual_seed(2024 + D)
-    x = torch.randint(0, hi, (N,), dtype=torch.int32, device="cuda", generator=g)
+    x = torch.randint(0, hi, (N,), dtype=dtype, device="cuda", generator=g)
     before = _props(x)
     hs.hs_sort(x, D, 8)
     torch.cuda.synchronize()
