@@ -66,7 +66,7 @@ def buckets(per_bucket, D, seed, dtype=np.int32, lo_frac=0.0, hi_frac=1.0):
     return k
 
 
-@pytest.mark.parametrize("c", [1, 2, 8])
+@pytest.mark.parametrize("c", [1, 2, 8, 64])
 def test_split_uniform_all_buckets(c):
     t = T(0)
     keys = buckets([c * 3 * t + 17 * b for b in range(10)], 9, 11 + c)
